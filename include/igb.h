@@ -1,0 +1,150 @@
+/*
+ * igb.h -- C ABI of the B200-native MG-PCG solve phase (libigb.so).
+ *
+ * The reference (igamg, pure Python/SciPy) has no native interface; each
+ * entry point below replaces the Python call that the reference's solve
+ * phase makes, so a host binding (ctypes / cffi / a C++ driver) can swap the
+ * CPU path for the device path one call at a time:
+ *
+ *   igb_set_level_matrix   <- MultigridSolver.__init__ storing A_l
+ *                             (reference pkg/src/igamg/multigrid.py:92-99)
+ *   igb_set_prolongation   <- assembly.prolongation / self.P[l]
+ *                             (assembly.py:672-702, multigrid.py:96)
+ *   igb_set_gs             <- smoothers.GaussSeidel.__init__ (smoothers.py:174-184)
+ *   igb_scms_add_interior  <- smoothers.ScmsInteriorSolver.__init__ (smoothers.py:232-281)
+ *   igb_scms_add_piece     <- SubspaceCorrectedMass piece factorizations (smoothers.py:316-319)
+ *   igb_set_coarse_lu      <- linsolve.factorize(A_0) (multigrid.py:100, linsolve.py:33-46)
+ *   igb_set_cycle          <- CycleConfig (multigrid.py:23-50) + build_smoother kind
+ *   igb_cycle              <- MultigridSolver.cycle (multigrid.py:118-138)
+ *   igb_pcg / igb_pcg_device <- linsolve.cg(A_L, b, preconditioner=cycle) (linsolve.py:64-101)
+ *   igb_op                 <- single hot-path operators for parity tests:
+ *                             A@x, f-A@u (scipy csr_matvec), GaussSeidel.apply_forward /
+ *                             apply_backward (smoothers.py:186-190),
+ *                             SubspaceCorrectedMass.apply (smoothers.py:321-325),
+ *                             P.T@r, P@e (multigrid.py:127,130,134),
+ *                             coarse_solver(r) (linsolve.py:48-53)
+ *
+ * Conventions: every function returns 0 on success and a negative code on
+ * failure (igb_last_error(ctx) gives a message).  Host pointers are borrowed
+ * for the duration of the call (data is copied).  All matrices are CSR with
+ * int32 indices and float64 values, rows with sorted column indices.  Level 0
+ * is the coarsest level; cycles act on levels >= 1 (multigrid.py:120-121).
+ * A context owns one CUDA stream and all device memory; it is not thread-safe.
+ */
+#ifndef IGB_H
+#define IGB_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct igb_ctx igb_ctx;
+
+enum {
+  IGB_OK = 0,
+  IGB_ERR_ARG = -1,
+  IGB_ERR_CUDA = -2,
+  IGB_ERR_STATE = -3,
+  IGB_ERR_SINGULAR = -4,
+  IGB_ERR_NOMEM = -5
+};
+
+/* smoother kinds (smoothers.py:356-367) */
+enum { IGB_SMOOTHER_GS = 0, IGB_SMOOTHER_SCMS = 1, IGB_SMOOTHER_HYBRID = 2 };
+
+/* operators for igb_op */
+enum {
+  IGB_OP_SPMV = 0,      /* out = A_l in                                   */
+  IGB_OP_RESIDUAL = 1,  /* out = out - A_l in  (out holds f on entry)      */
+  IGB_OP_GS_FWD = 2,    /* out = tril(A_l)^{-1} in                          */
+  IGB_OP_GS_BWD = 3,    /* out = tril(A_l)^{-T} in                          */
+  IGB_OP_SCMS = 4,      /* out = tau * sum_T P_T L_T^{-1} P_T^T in          */
+  IGB_OP_RESTRICT = 5,  /* out = P_l^T in   (in: n_l, out: n_{l-1})         */
+  IGB_OP_PROLONG = 6,   /* out = P_l in     (in: n_{l-1}, out: n_l)         */
+  IGB_OP_COARSE = 7,    /* out = A_0^{-1} in (level ignored)                */
+  IGB_OP_CYCLE = 8      /* out = cycle(l, in) from u = 0                    */
+};
+
+int igb_create(igb_ctx** ctx, int device);
+int igb_destroy(igb_ctx* ctx);
+const char* igb_last_error(igb_ctx* ctx);
+int igb_version(void);
+
+/* Hierarchy with levels 0..L (L >= 1). Must be called first. */
+int igb_set_num_levels(igb_ctx* ctx, int L);
+
+/* A_l (l = 0..L): n x n CSR. */
+int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz,
+                         const int* indptr, const int* indices, const double* data);
+
+/* P_l (l = 1..L): n_l x n_{l-1} CSR; the transpose for restriction is built here. */
+int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long long nnz,
+                         const int* indptr, const int* indices, const double* data);
+
+/* Gauss-Seidel on A_l in natural order (level schedules are built here). */
+int igb_set_gs(igb_ctx* ctx, int level);
+
+/* SCMS smoother of level l: damping tau; then interiors and interface pieces. */
+int igb_scms_begin(igb_ctx* ctx, int level, double tau);
+/* One patch interior: dim in {2,3}; dims[a] = n_a; T_a is n_a x n_a row-major
+ * (columns = eigenvectors of the split subspaces, [W_L V_L | W_C V_C]);
+ * denom has prod(n_a) entries (C order); idx maps the C-order tensor to free ids.
+ * T2 is ignored when dim == 2. Interiors sharing T/denom pointers share storage. */
+int igb_scms_add_interior(igb_ctx* ctx, int level, int dim, const int* dims,
+                          const double* T0, const double* T1, const double* T2,
+                          const double* denom, const int* idx);
+/* One interface piece (edge/face/vertex): m free ids and the dense inverse
+ * (m x m row-major) of A_l[idx][:, idx]. */
+int igb_scms_add_piece(igb_ctx* ctx, int level, int m, const int* idx, const double* inv);
+
+/* Coarse solver from SciPy SuperLU factors of A_0: Pr A Pc = L U with
+ * Pr[perm_r[i], i] = 1, Pc[i, perm_c[i]] = 1. L, U given as CSR (n0 x n0). */
+int igb_set_coarse_lu(igb_ctx* ctx, int n0,
+                      long long l_nnz, const int* l_ptr, const int* l_idx, const double* l_val,
+                      long long u_nnz, const int* u_ptr, const int* u_idx, const double* u_val,
+                      const int* perm_r, const int* perm_c);
+
+/* Cycle shape: smoother kind, mu (1 = V, 2 = W), steps per level (L+1 entries, index = level). */
+int igb_set_cycle(igb_ctx* ctx, int smoother, int mu, const int* steps_per_level);
+
+/* Upload done: validates the hierarchy and captures the cycle as a CUDA graph. */
+int igb_finalize(igb_ctx* ctx);
+
+/* One cycle on level l from u = 0 (host buffers of length n_l). */
+int igb_cycle(igb_ctx* ctx, int level, const double* f, double* u);
+
+/* Single operator (host buffers). */
+int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out);
+
+/* Preconditioned CG on A_L with one cycle as preconditioner, x0 = 0
+ * (linsolve.py:64-101 semantics). Host buffers: b, x (length n_L), hist
+ * (capacity hist_cap; hist[i] = ||r_{i+1}|| / ||b||). *its receives the
+ * iteration count (max_iters if not converged). */
+int igb_pcg(igb_ctx* ctx, const double* b, double tol, int max_iters,
+            double* x, int* its, double* hist, int hist_cap);
+
+/* Same with device-resident b and x (device pointers); hist stays a host buffer. */
+int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
+                   double* d_x, int* its, double* hist, int hist_cap);
+
+/* Device scratch helpers for device-resident benchmarking. */
+int igb_device_alloc(igb_ctx* ctx, long long bytes, void** dptr);
+int igb_device_free(igb_ctx* ctx, void* dptr);
+int igb_memcpy_h2d(igb_ctx* ctx, void* dst, const void* src, long long bytes);
+int igb_memcpy_d2h(igb_ctx* ctx, void* dst, const void* src, long long bytes);
+
+/* Device milliseconds (CUDA events) of the last igb_pcg / igb_pcg_device CG loop,
+ * and the average device time of one cycle in it. */
+int igb_last_timing(igb_ctx* ctx, double* pcg_ms, double* cycle_ms_avg);
+
+/* Per-kernel-class accumulated device time (ms) and launch counts since
+ * igb_profile_reset; classes: 0 spmv, 1 gs, 2 fd, 3 pieces, 4 transfer,
+ * 5 coarse, 6 cg-vector. Enabled by igb_profile_enable(ctx, 1). */
+int igb_profile_enable(igb_ctx* ctx, int on);
+int igb_profile_reset(igb_ctx* ctx);
+int igb_profile_get(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IGB_H */

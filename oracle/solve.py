@@ -1,0 +1,251 @@
+"""CPU oracle of the MG-PCG solve phase -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py`` (its
+``cpu_baseline`` leg and ``--impl reference`` arm) may import this module, and
+only as the checker / the timed CPU reference.  The product package
+``paper_1902_01818_b200`` never imports it and has no CPU fallback.
+
+It restates the reference's solve phase operation for operation with the same
+third-party calls, so that on identical setup data it reproduces the
+reference bit for bit (pinned in ``tests/test_oracle.py`` against the
+reference itself and against ``tests/golden/*.npz``):
+
+* ``cg``                         <- ``linsolve.cg``            (pkg/src/igamg/linsolve.py:64-101)
+* ``OracleSolver.cycle``         <- ``MultigridSolver.cycle``  (multigrid.py:118-138)
+* ``OracleSolver.check_spd``     <- ``check_preconditioner_spd`` (multigrid.py:144-159)
+* ``_GaussSeidel``               <- ``smoothers.GaussSeidel``  (smoothers.py:171-200)
+* ``_interior_solve``            <- ``ScmsInteriorSolver.solve`` (smoothers.py:283-294)
+* ``_Scms.apply``                <- ``SubspaceCorrectedMass.apply`` (smoothers.py:321-325)
+* hybrid pre/post smoothing      <- ``HybridSmoother``         (smoothers.py:343-353)
+* coarse / piece solves          <- ``linsolve.Factorization.solve`` (linsolve.py:33-53)
+
+Input is a *setup bundle* (plain dict: matrices ``A``, prolongations ``P``,
+smoother kind, ``mu``, steps per level, per-level SCMS interior/piece data),
+produced either by the product's host setup (``MultigridSetup.setup_bundle``)
+or extracted from a reference ``MultigridSolver`` (``bundle_from_reference``).
+"""
+
+import numpy as np
+import scipy.sparse
+import scipy.sparse.linalg
+
+__all__ = ["cg", "OracleSolver", "bundle_from_reference"]
+
+
+def cg(A, b, preconditioner=None, tol=1e-8, max_iters=10000, callback=None):
+    """PCG with recursive residual; returns (x, iterations, history) (linsolve.py:64-101)."""
+    b = np.asarray(b, dtype=float)
+    n = b.shape[0]
+    normb = np.linalg.norm(b)
+    x = np.zeros(n)
+    if normb == 0.0:
+        return x, 0, []
+    apply_prec = preconditioner if preconditioner is not None else (lambda r: r)
+    r = b.copy()
+    z = apply_prec(r)
+    d = z.copy()
+    rz = r @ z
+    history = []
+    for it in range(1, max_iters + 1):
+        Ad = A @ d
+        alpha = rz / (d @ Ad)
+        x += alpha * d
+        r -= alpha * Ad
+        rel = np.linalg.norm(r) / normb
+        history.append(rel)
+        if callback is not None:
+            callback(it, rel)
+        if rel <= tol:
+            return x, it, history
+        z = apply_prec(r)
+        rz_new = r @ z
+        beta = rz_new / rz
+        rz = rz_new
+        d = z + beta * d
+    return x, max_iters, history
+
+
+def _splu_spd(A):
+    """SuperLU with SciPy defaults (COLAMD, partial pivoting) as linsolve.Factorization does."""
+    return scipy.sparse.linalg.splu(scipy.sparse.csc_matrix(A))
+
+
+class _GaussSeidel:
+    def __init__(self, A):
+        A = A.tocsr()
+        if np.any(A.diagonal() == 0.0):
+            raise ValueError("Gauss-Seidel needs a nonzero diagonal")
+        tril = scipy.sparse.tril(A, format="csc")
+        self._lu = scipy.sparse.linalg.splu(
+            tril, permc_spec="NATURAL", diag_pivot_thresh=0.0, options={"SymmetricMode": True})
+
+    def forward(self, r):
+        return self._lu.solve(r, trans="N")
+
+    def backward(self, r):
+        return self._lu.solve(r, trans="T")
+
+
+def _interior_solve(subspaces, dims, r):
+    R = np.asarray(r).reshape(dims)
+    out = np.zeros_like(R)
+    for Ts, denom in subspaces:
+        Y = R
+        for a, T in enumerate(Ts):
+            Y = np.moveaxis(np.tensordot(T.T, Y, axes=(1, a)), 0, a)
+        Y = Y / denom
+        for a, T in enumerate(Ts):
+            Y = np.moveaxis(np.tensordot(T, Y, axes=(1, a)), 0, a)
+        out += Y
+    return out.ravel()
+
+
+class _Scms:
+    def __init__(self, A, entry):
+        self.tau = entry["tau"]
+        self._solvers = []
+        for it in entry["interiors"]:
+            subs, dims = it["subspaces"], tuple(it["dims"])
+            self._solvers.append((it["indices"], lambda r, s=subs, d=dims: _interior_solve(s, d, r)))
+        A = A.tocsr()
+        for idx in entry["pieces"]:
+            lu = _splu_spd(A[idx][:, idx].tocsc())
+            self._solvers.append((idx, lambda b, lu=lu: lu.solve(np.asarray(b, dtype=float), trans="N")))
+
+    def apply(self, r):
+        out = np.zeros_like(r)
+        for indices, solve in self._solvers:
+            out[indices] += solve(r[indices])
+        return self.tau * out
+
+
+class OracleSolver:
+    """Reference-faithful cycle / preconditioner on a setup bundle."""
+
+    def __init__(self, bundle):
+        self.A = bundle["A"]
+        self.P = bundle["P"]
+        self.kind = bundle["smoother"]
+        self.mu = bundle["mu"]
+        self.steps = bundle["steps"]
+        self.finest = bundle["finest"]
+        self.coarse = _splu_spd(self.A[0])
+        self.gs = [None] * (self.finest + 1)
+        self.scms = [None] * (self.finest + 1)
+        for level in range(1, self.finest + 1):
+            if self.kind in ("gs", "hyb"):
+                self.gs[level] = _GaussSeidel(self.A[level])
+            if self.kind in ("scms", "hyb"):
+                self.scms[level] = _Scms(self.A[level], bundle["levels"][level])
+
+    @property
+    def n_dofs(self):
+        return self.A[self.finest].shape[0]
+
+    def _pre(self, level, A, u, f, steps):
+        gs, scms = self.gs[level], self.scms[level]
+        if self.kind == "gs":
+            for _ in range(steps):
+                u += gs.forward(f - A @ u)
+        elif self.kind == "scms":
+            for _ in range(steps):
+                u += scms.apply(f - A @ u)
+        else:
+            u += gs.forward(f - A @ u)
+            for _ in range(steps):
+                u += scms.apply(f - A @ u)
+        return u
+
+    def _post(self, level, A, u, f, steps):
+        gs, scms = self.gs[level], self.scms[level]
+        if self.kind == "gs":
+            for _ in range(steps):
+                u += gs.backward(f - A @ u)
+        elif self.kind == "scms":
+            for _ in range(steps):
+                u += scms.apply(f - A @ u)
+        else:
+            for _ in range(steps):
+                u += scms.apply(f - A @ u)
+            u += gs.backward(f - A @ u)
+        return u
+
+    def cycle(self, level, f, u=None):
+        if level < 1:
+            raise ValueError("cycles act on levels >= 1")
+        A = self.A[level]
+        u = np.zeros_like(f) if u is None else u
+        steps = self.steps[level]
+        u = self._pre(level, A, u, f, steps)
+        r = self.P[level].T @ (f - A @ u)
+        if level == 1:
+            u = u + self.P[level] @ self.coarse.solve(np.asarray(r, dtype=float), trans="N")
+        else:
+            for _ in range(self.mu):
+                correction = self.cycle(level - 1, r)
+                u = u + self.P[level] @ correction
+                if self.mu > 1:
+                    r = self.P[level].T @ (f - A @ u)
+        return self._post(level, A, u, f, steps)
+
+    def preconditioner(self):
+        return lambda r: self.cycle(self.finest, r)
+
+    # single operators, for per-kernel parity tests
+    def gs_forward(self, level, r):
+        return self.gs[level].forward(r)
+
+    def gs_backward(self, level, r):
+        return self.gs[level].backward(r)
+
+    def scms_apply(self, level, r):
+        return self.scms[level].apply(r)
+
+    def coarse_solve(self, r):
+        return self.coarse.solve(np.asarray(r, dtype=float), trans="N")
+
+    def check_spd(self, rtol=1e-8, seed=20240801):
+        rng = np.random.default_rng(seed)
+        r = rng.standard_normal(self.n_dofs)
+        s = rng.standard_normal(self.n_dofs)
+        Br, Bs = self.cycle(self.finest, r), self.cycle(self.finest, s)
+        lhs, rhs = s @ Br, r @ Bs
+        scale = max(abs(lhs), abs(rhs), 1e-30)
+        return abs(lhs - rhs) <= rtol * scale and r @ Br > 0 and s @ Bs > 0
+
+    def solve(self, b, tol=1e-8, max_iters=500):
+        return cg(self.A[self.finest], b, self.preconditioner(), tol=tol, max_iters=max_iters)
+
+
+def bundle_from_reference(solver):
+    """Setup bundle extracted from a *reference* ``igamg.multigrid.MultigridSolver``.
+
+    Used only to pin the oracle against the reference in this container
+    (SURVEY.md Appendix A "Adapter").
+    """
+    cfg = solver.config
+    L = solver.finest
+    levels = [None]
+    for level in range(1, L + 1):
+        smo = solver.smoother[level]
+        scms = getattr(smo, "scms", None)
+        if scms is None and hasattr(smo, "decomposition"):
+            scms = smo
+        entry = {}
+        if scms is not None:
+            entry["tau"] = scms.tau
+            interiors, pieces = [], []
+            for indices, solve in scms._solvers:
+                owner = getattr(solve, "__self__", None)
+                if owner is not None and hasattr(owner, "_subspaces"):
+                    interiors.append({"indices": indices, "dims": owner.dims,
+                                      "subspaces": owner._subspaces})
+                else:
+                    pieces.append(indices)
+            entry["interiors"] = interiors
+            entry["pieces"] = pieces
+        levels.append(entry)
+    return {
+        "A": list(solver.A), "P": list(solver.P), "smoother": cfg.smoother, "mu": cfg.mu,
+        "steps": [cfg.steps_at(l, L) for l in range(L + 1)], "levels": levels, "finest": L,
+    }

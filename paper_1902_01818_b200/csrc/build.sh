@@ -1,0 +1,14 @@
+#!/usr/bin/env bash
+# Build libigb.so (sm_100a) in-tree. Usage: csrc/build.sh [out.so]
+set -euo pipefail
+HERE="$(cd "$(dirname "$0")" && pwd)"
+PKG="$(dirname "$HERE")"
+ROOT="$(dirname "$PKG")"
+OUT="${1:-$PKG/libigb.so}"
+NVCC="${NVCC:-nvcc}"
+"$NVCC" -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
+  -Xcompiler -fPIC -Xcompiler -Wall -shared -I"$ROOT/include" -I"$HERE" \
+  ${IGB_NVCC_EXTRA:-} \
+  -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/igb.cu"
+mv "$OUT.tmp" "$OUT"
+echo "built $OUT"

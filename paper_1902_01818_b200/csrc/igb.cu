@@ -1,0 +1,1144 @@
+// igb.cu -- native runtime of the device MG-PCG solve: context, device memory,
+// Gauss-Seidel level schedules, cycle orchestration (captured as a CUDA graph),
+// PCG driver and the C ABI declared in include/igb.h.
+//
+// Cycle semantics follow the reference exactly (pkg/src/igamg/multigrid.py:118-138,
+// smoothers.py:186-200, 321-353):
+//   u = 0; pre_smooth; r = P^T (f - A u); coarse (l == 1) or mu recursive cycles,
+//   each followed by u = u + P e; post_smooth.
+// A "u is still zero" flag is tracked so that f - A*0 is never computed (bitwise
+// identical shortcut: the reference computes f - A@0 == f).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "igb.h"
+#include "kernels.cuh"
+
+using namespace igb;
+
+namespace {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ArgError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CU(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess)                                                              \
+      throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+  } while (0)
+
+enum KernelClass { K_SPMV = 0, K_GS = 1, K_FD = 2, K_PIECES = 3, K_TRANSFER = 4, K_COARSE = 5, K_CG = 6, K_NCLASS = 7 };
+
+struct DevCsr {
+  int n = 0, m = 0;
+  long long nnz = 0;
+  int* ptr = nullptr;
+  int* col = nullptr;
+  double* val = nullptr;
+  int group = 8;
+};
+
+struct Sched {
+  int nlev = 0;
+  int* lvl_ptr = nullptr;
+  int* rows = nullptr;
+};
+
+struct InteriorStage {
+  int dim;
+  int n[3];
+  const double* T[3];   // device
+  const double* D;      // device
+  const int* idx;       // device
+};
+
+struct FdPlan {
+  int nsteps = 0;
+  GemmDesc* d_desc[6] = {nullptr};
+  int ndesc[6] = {0};
+  int tiles[6] = {0};
+  double bytes[6] = {0};
+  int first_gather = 0;   // step index with the gather
+  int last_scatter = 0;   // step index with the scatter
+};
+
+struct Level {
+  int n = 0;
+  DevCsr A;
+  std::vector<int> h_ptr, h_col;
+  std::vector<double> h_diag;
+  int* dpos = nullptr;
+  bool has_P = false;
+  DevCsr P, PT;
+  bool has_gs = false;
+  Sched fwd, bwd;
+  long long tri_nnz_lower = 0, tri_nnz_upper = 0;
+  bool has_scms = false;
+  double tau = 1.0;
+  std::vector<InteriorStage> interiors;
+  std::vector<PieceRowBlock> h_blocks;
+  PieceRowBlock* d_blocks = nullptr;
+  double piece_bytes = 0;
+  long long piece_rows = 0;
+  FdPlan fd;
+  size_t fd_scratch = 0;
+  double* f = nullptr;
+  double* u = nullptr;
+  double* r = nullptr;
+  double* c = nullptr;
+  double* s0 = nullptr;
+  double* s1 = nullptr;
+};
+
+struct Coarse {
+  bool set = false;
+  int n = 0;
+  DevCsr L, U;
+  int *Ldpos = nullptr, *Udpos = nullptr;
+  Sched Ls, Us;
+  int* inv_perm_r = nullptr;
+  int* perm_c = nullptr;
+  double* y = nullptr;
+  double* w = nullptr;
+};
+
+struct ProfRec {
+  int cls;
+  double bytes;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+
+struct igb_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  int L = -1;
+  std::vector<Level> lev;
+  Coarse coarse;
+  int smoother = IGB_SMOOTHER_HYBRID;
+  int mu = 1;
+  std::vector<int> steps;
+  bool finalized = false;
+  std::vector<void*> allocs;
+  std::map<const void*, void*> shared_uploads;  // host pointer -> device copy (FD data)
+
+  // CG state
+  double *x = nullptr, *d = nullptr, *q = nullptr, *b = nullptr, *partials = nullptr,
+         *hist_dev = nullptr;
+  unsigned* counter = nullptr;
+  CgScalars* sc = nullptr;
+  CgScalars* sc_host = nullptr;  // pinned
+  int hist_cap = 0;
+
+  // graph of cycle(L)
+  cudaGraphExec_t cycle_exec = nullptr;
+  bool capturing = false;
+  bool graph_prof = false;
+
+  // profiling
+  bool prof = false;
+  std::vector<ProfRec> direct_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  size_t ev_next = 0;
+  std::vector<ProfRec> graph_recs;
+  double prof_ms[K_NCLASS] = {0};
+  long long prof_n[K_NCLASS] = {0};
+  double prof_bytes[K_NCLASS] = {0};
+
+  // timing of last pcg
+  double last_pcg_ms = 0, last_cycle_ms = 0;
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+
+  template <class T>
+  T* alloc(size_t count) {
+    if (count == 0) count = 1;
+    void* p = nullptr;
+    CU(cudaMalloc(&p, count * sizeof(T)));
+    allocs.push_back(p);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const T* h, size_t count) {
+    T* p = alloc<T>(count);
+    if (count) CU(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    return p;
+  }
+
+  cudaEvent_t pool_event() {
+    if (ev_next == ev_pool.size()) {
+      cudaEvent_t e;
+      CU(cudaEventCreate(&e));
+      ev_pool.push_back(e);
+    }
+    return ev_pool[ev_next++];
+  }
+
+  // Launch wrapper: records CUDA events around the launch in profile mode.
+  template <class F>
+  void launch(int cls, double bytes, F&& f) {
+    if (!prof) {
+      f();
+      return;
+    }
+    ProfRec r{cls, bytes, nullptr, nullptr};
+    if (capturing) {
+      CU(cudaEventCreate(&r.a));
+      CU(cudaEventCreate(&r.b));
+    } else {
+      r.a = pool_event();
+      r.b = pool_event();
+    }
+    CU(cudaEventRecord(r.a, stream));
+    f();
+    CU(cudaEventRecord(r.b, stream));
+    (capturing ? graph_recs : direct_recs).push_back(r);
+  }
+  void harvest(std::vector<ProfRec>& recs, bool clear) {
+    for (auto& r : recs) {
+      float ms = 0;
+      CU(cudaEventElapsedTime(&ms, r.a, r.b));
+      prof_ms[r.cls] += ms;
+      prof_n[r.cls] += 1;
+      prof_bytes[r.cls] += r.bytes;
+    }
+    if (clear) {
+      recs.clear();
+      ev_next = 0;
+    }
+  }
+  void drop_graph() {
+    if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
+    cycle_exec = nullptr;
+    for (auto& r : graph_recs) {
+      cudaEventDestroy(r.a);
+      cudaEventDestroy(r.b);
+    }
+    graph_recs.clear();
+  }
+
+  // ---------------------------------------------------------------- operators
+  Level& level(int l) {
+    if (l < 0 || l > L) throw ArgError("level out of range");
+    return lev[l];
+  }
+
+  void spmv(const DevCsr& M, const double* x_, const double* z, double* y, int sign, int cls) {
+    const double bytes = 12.0 * M.nnz + 4.0 * (M.n + 1) + 8.0 * M.m + 8.0 * M.n + (sign ? 8.0 * M.n : 0.0);
+    launch(cls, bytes, [&] { launch_spmv(stream, M.n, M.ptr, M.col, M.val, x_, z, y, sign, M.group); });
+  }
+
+  // GS correction on level l: solve tril (fwd) / triu (bwd); if into_u_zero the
+  // solution is written straight into u (u was zero), else c is solved and
+  // accumulated into u.
+  void gs(int l, bool upper, const double* rhs, double* u, bool u_zero) {
+    Level& V = lev[l];
+    TrsvPhase ph{};
+    const Sched& S = upper ? V.bwd : V.fwd;
+    ph.nlev = S.nlev;
+    ph.lvl_ptr = S.lvl_ptr;
+    ph.rows = S.rows;
+    ph.ptr = V.A.ptr;
+    ph.col = V.A.col;
+    ph.val = V.A.val;
+    ph.dpos = V.dpos;
+    ph.upper = upper ? 1 : 0;
+    ph.rhs = rhs;
+    ph.rhs_idx = nullptr;
+    if (u_zero) {
+      ph.x = u;
+      ph.uacc = nullptr;
+    } else {
+      ph.x = V.c;
+      ph.uacc = u;
+    }
+    const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+    const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
+    launch(K_GS, bytes, [&] { launch_sptrsv(stream, ph, nullptr, 0, nullptr, nullptr); });
+  }
+
+  // u (+)= tau * SCMS(res)
+  void scms(int l, const double* res, double* u, bool u_zero) {
+    Level& V = lev[l];
+    const FdPlan& F = V.fd;
+    for (int s = 0; s < F.nsteps; ++s) {
+      if (F.ndesc[s] == 0) continue;
+      launch(K_FD, F.bytes[s], [&] {
+        launch_fd_gemm(stream, F.d_desc[s], F.ndesc[s], F.tiles[s], res, u, V.tau, u_zero ? 0 : 1);
+      });
+    }
+    if (!V.h_blocks.empty()) {
+      launch(K_PIECES, V.piece_bytes, [&] {
+        launch_piece_gemv(stream, V.d_blocks, (int)V.h_blocks.size(), res, u, V.tau, u_zero ? 0 : 1);
+      });
+    }
+  }
+
+  void coarse_solve(const double* rhs, double* out) {
+    Coarse& C = coarse;
+    TrsvPhase a{}, b{};
+    a.nlev = C.Ls.nlev; a.lvl_ptr = C.Ls.lvl_ptr; a.rows = C.Ls.rows;
+    a.ptr = C.L.ptr; a.col = C.L.col; a.val = C.L.val; a.dpos = C.Ldpos; a.upper = 0;
+    a.rhs = rhs; a.rhs_idx = C.inv_perm_r; a.x = C.y; a.uacc = nullptr;
+    b.nlev = C.Us.nlev; b.lvl_ptr = C.Us.lvl_ptr; b.rows = C.Us.rows;
+    b.ptr = C.U.ptr; b.col = C.U.col; b.val = C.U.val; b.dpos = C.Udpos; b.upper = 1;
+    b.rhs = C.y; b.rhs_idx = nullptr; b.x = C.w; b.uacc = nullptr;
+    const double bytes = 12.0 * (C.L.nnz + C.U.nnz) + 8.0 * (C.L.n + 1) + 40.0 * C.n;
+    launch(K_COARSE, bytes, [&] { launch_sptrsv(stream, a, &b, C.n, C.perm_c, out); });
+  }
+
+  void residual(int l, const double* f, const double* u, double* r) {
+    spmv(lev[l].A, u, f, r, -1, K_SPMV);
+  }
+
+  // One smoothing step kind: 'G' fwd GS, 'B' bwd GS, 'S' scms
+  void smooth_step(int l, char kind, const double* f, double* u, bool& u_zero) {
+    Level& V = lev[l];
+    const double* res = f;
+    if (!u_zero) {
+      residual(l, f, u, V.r);
+      res = V.r;
+    }
+    if (kind == 'S') scms(l, res, u, u_zero);
+    else gs(l, kind == 'B', res, u, u_zero);
+    u_zero = false;
+  }
+
+  void pre_smooth(int l, const double* f, double* u, bool& uz) {
+    const int st = steps[l];
+    if (smoother == IGB_SMOOTHER_GS) {
+      for (int i = 0; i < st; ++i) smooth_step(l, 'G', f, u, uz);
+    } else if (smoother == IGB_SMOOTHER_SCMS) {
+      for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
+    } else {
+      smooth_step(l, 'G', f, u, uz);
+      for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
+    }
+  }
+  void post_smooth(int l, const double* f, double* u, bool& uz) {
+    const int st = steps[l];
+    if (smoother == IGB_SMOOTHER_GS) {
+      for (int i = 0; i < st; ++i) smooth_step(l, 'B', f, u, uz);
+    } else if (smoother == IGB_SMOOTHER_SCMS) {
+      for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
+    } else {
+      for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
+      smooth_step(l, 'B', f, u, uz);
+    }
+  }
+
+  void restrict_residual(int l, const double* f, const double* u, bool uz, double* fc) {
+    Level& V = lev[l];
+    const double* res = f;
+    if (!uz) {
+      residual(l, f, u, V.r);
+      res = V.r;
+    }
+    spmv(V.PT, res, nullptr, fc, 0, K_TRANSFER);
+  }
+
+  // cycle on level l: f -> u (u overwritten)
+  void cycle(int l, const double* f, double* u) {
+    Level& V = lev[l];
+    bool uz = true;
+    pre_smooth(l, f, u, uz);
+    Level& C = lev[l - 1];
+    restrict_residual(l, f, u, uz, C.f);
+    if (l == 1) {
+      coarse_solve(C.f, C.u);
+      spmv(V.P, C.u, uz ? nullptr : u, u, uz ? 0 : 1, K_TRANSFER);
+      uz = false;
+    } else {
+      for (int k = 0; k < mu; ++k) {
+        cycle(l - 1, C.f, C.u);
+        spmv(V.P, C.u, uz ? nullptr : u, u, uz ? 0 : 1, K_TRANSFER);
+        uz = false;
+        if (mu > 1) restrict_residual(l, f, u, uz, C.f);
+      }
+    }
+    post_smooth(l, f, u, uz);
+  }
+
+  void run_finest_cycle() {
+    // cycle(L): lev[L].f -> lev[L].u, replayed from a CUDA graph
+    if (!cycle_exec || graph_prof != prof) {
+      drop_graph();
+      cudaGraph_t g;
+      capturing = true;
+      CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      try {
+        cycle(L, lev[L].f, lev[L].u);
+      } catch (...) {
+        cudaStreamEndCapture(stream, &g);
+        capturing = false;
+        throw;
+      }
+      CU(cudaStreamEndCapture(stream, &g));
+      capturing = false;
+      CU(cudaGraphInstantiate(&cycle_exec, g, 0));
+      CU(cudaGraphDestroy(g));
+      graph_prof = prof;
+    }
+    CU(cudaGraphLaunch(cycle_exec, stream));
+  }
+  void harvest_graph() {
+    if (prof && !graph_recs.empty()) harvest(graph_recs, false);
+  }
+};
+
+namespace {
+
+int fail(igb_ctx* ctx, int code, const std::string& msg) {
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(igb_ctx* ctx, F&& f) {
+  if (!ctx) return IGB_ERR_ARG;
+  try {
+    f();
+    return IGB_OK;
+  } catch (const ArgError& e) {
+    return fail(ctx, IGB_ERR_ARG, e.what());
+  } catch (const StateError& e) {
+    return fail(ctx, IGB_ERR_STATE, e.what());
+  } catch (const CudaError& e) {
+    return fail(ctx, IGB_ERR_CUDA, e.what());
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, IGB_ERR_NOMEM, "host allocation failed");
+  } catch (const std::exception& e) {
+    return fail(ctx, IGB_ERR_STATE, e.what());
+  }
+}
+
+int pick_group(long long nnz, int n) {
+  const double avg = n ? double(nnz) / n : 0;
+  if (avg <= 6) return 4;
+  if (avg <= 14) return 8;
+  if (avg <= 40) return 16;
+  return 32;
+}
+
+void check_csr(int n, int m, long long nnz, const int* ptr, const int* idx) {
+  if (n < 0 || m < 0 || nnz < 0) throw ArgError("negative dimension");
+  if (!ptr || (nnz && !idx)) throw ArgError("null CSR array");
+  if (ptr[0] != 0 || ptr[n] != nnz) throw ArgError("indptr does not match nnz");
+  for (int i = 0; i < n; ++i) {
+    if (ptr[i + 1] < ptr[i]) throw ArgError("indptr not monotone");
+    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+      if (idx[k] < 0 || idx[k] >= m) throw ArgError("column index out of range");
+      if (k > ptr[i] && idx[k] <= idx[k - 1]) throw ArgError("column indices must be sorted and unique");
+    }
+  }
+}
+
+DevCsr upload_csr(igb_ctx* ctx, int n, int m, long long nnz, const int* ptr, const int* idx,
+                  const double* val) {
+  DevCsr c;
+  c.n = n;
+  c.m = m;
+  c.nnz = nnz;
+  c.ptr = ctx->upload(ptr, (size_t)n + 1);
+  c.col = ctx->upload(idx, (size_t)nnz);
+  c.val = ctx->upload(val, (size_t)nnz);
+  c.group = pick_group(nnz, n);
+  return c;
+}
+
+// Diagonal position per row (must exist and be nonzero).
+std::vector<int> diag_positions(int n, const int* ptr, const int* col, const double* val,
+                                const char* what) {
+  std::vector<int> dp(n);
+  for (int i = 0; i < n; ++i) {
+    const int* b = col + ptr[i];
+    const int* e = col + ptr[i + 1];
+    const int* it = std::lower_bound(b, e, i);
+    if (it == e || *it != i) throw ArgError(std::string(what) + ": missing diagonal entry");
+    dp[i] = int(it - col);
+    if (val && val[dp[i]] == 0.0) throw ArgError(std::string(what) + ": zero diagonal entry");
+  }
+  return dp;
+}
+
+// Level sets of the lower (col < row) or upper (col > row) triangle.
+Sched build_schedule(igb_ctx* ctx, int n, const int* ptr, const int* col, const std::vector<int>& dp,
+                     bool upper) {
+  std::vector<int> lv(n, 0);
+  int maxl = -1;
+  if (!upper) {
+    for (int i = 0; i < n; ++i) {
+      int l = 0;
+      for (int k = ptr[i]; k < dp[i]; ++k) l = std::max(l, lv[col[k]] + 1);
+      lv[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  } else {
+    for (int i = n - 1; i >= 0; --i) {
+      int l = 0;
+      for (int k = dp[i] + 1; k < ptr[i + 1]; ++k) l = std::max(l, lv[col[k]] + 1);
+      lv[i] = l;
+      maxl = std::max(maxl, l);
+    }
+  }
+  const int nlev = maxl + 1;
+  std::vector<int> cnt(nlev + 1, 0), rows(n);
+  for (int i = 0; i < n; ++i) cnt[lv[i] + 1]++;
+  for (int l = 0; l < nlev; ++l) cnt[l + 1] += cnt[l];
+  std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+  for (int i = 0; i < n; ++i) rows[pos[lv[i]]++] = i;
+  Sched s;
+  s.nlev = nlev;
+  s.lvl_ptr = ctx->upload(cnt.data(), cnt.size());
+  s.rows = ctx->upload(rows.data(), rows.size());
+  return s;
+}
+
+void require_levels(igb_ctx* ctx) {
+  if (ctx->L < 1) throw StateError("igb_set_num_levels must be called first");
+}
+
+void require_final(igb_ctx* ctx) {
+  if (!ctx->finalized) throw StateError("igb_finalize has not been called");
+}
+
+void build_fd_plan(igb_ctx* ctx, Level& V) {
+  if (V.interiors.empty()) return;
+  size_t total = 0;
+  int dim = V.interiors[0].dim;
+  for (auto& it : V.interiors) {
+    if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
+    total += (size_t)it.n[0] * it.n[1] * (dim == 3 ? it.n[2] : 1);
+  }
+  V.fd_scratch = total;
+  V.s0 = ctx->alloc<double>(total);
+  V.s1 = ctx->alloc<double>(total);
+  FdPlan& F = V.fd;
+  F.nsteps = dim == 2 ? 4 : 6;
+  std::vector<std::vector<GemmDesc>> steps(F.nsteps);
+  size_t base = 0;
+  for (auto& it : V.interiors) {
+    const long long n0 = it.n[0], n1 = it.n[1], n2 = dim == 3 ? it.n[2] : 1;
+    double* B0 = V.s0 + base;
+    double* B1 = V.s1 + base;
+    auto mk = [](int M, int N, int K, int nb) {
+      GemmDesc g{};
+      g.M = M; g.N = N; g.K = K; g.nb = nb;
+      return g;
+    };
+    if (dim == 2) {
+      GemmDesc g = mk(n0, n1, n0, 1);  // Z = T0^T R   (R gathered)
+      g.A = it.T[0]; g.a_rs = 1; g.a_cs = n0;
+      g.b_idx = it.idx; g.b_rs = n1; g.b_cs = 1;
+      g.C = B0; g.c_rs = n1; g.c_cs = 1;
+      steps[0].push_back(g);
+      g = mk(n0, n1, n1, 1);  // Y = Z T1 / D
+      g.A = B0; g.a_rs = n1; g.a_cs = 1;
+      g.B = it.T[1]; g.b_rs = n1; g.b_cs = 1;
+      g.C = B1; g.c_rs = n1; g.c_cs = 1; g.D = it.D;
+      steps[1].push_back(g);
+      g = mk(n0, n1, n0, 1);  // W = T0 Y
+      g.A = it.T[0]; g.a_rs = n0; g.a_cs = 1;
+      g.B = B1; g.b_rs = n1; g.b_cs = 1;
+      g.C = B0; g.c_rs = n1; g.c_cs = 1;
+      steps[2].push_back(g);
+      g = mk(n0, n1, n1, 1);  // X = W T1^T -> u[idx] (+)= tau X
+      g.A = B0; g.a_rs = n1; g.a_cs = 1;
+      g.B = it.T[1]; g.b_rs = 1; g.b_cs = n1;
+      g.c_idx = it.idx; g.c_rs = n1; g.c_cs = 1;
+      steps[3].push_back(g);
+    } else {
+      const long long n12 = n1 * n2, n01 = n0 * n1;
+      GemmDesc g = mk(n0, n12, n0, 1);  // mode 0 fwd (gather)
+      g.A = it.T[0]; g.a_rs = 1; g.a_cs = n0;
+      g.b_idx = it.idx; g.b_rs = n12; g.b_cs = 1;
+      g.C = B0; g.c_rs = n12; g.c_cs = 1;
+      steps[0].push_back(g);
+      g = mk(n1, n2, n1, n0);  // mode 1 fwd, batched over i0
+      g.A = it.T[1]; g.a_rs = 1; g.a_cs = n1; g.a_bs = 0;
+      g.B = B0; g.b_rs = n2; g.b_cs = 1; g.b_bs = n12;
+      g.C = B1; g.c_rs = n2; g.c_cs = 1; g.c_bs = n12;
+      steps[1].push_back(g);
+      g = mk(n01, n2, n2, 1);  // mode 2 fwd, divide
+      g.A = B1; g.a_rs = n2; g.a_cs = 1;
+      g.B = it.T[2]; g.b_rs = n2; g.b_cs = 1;
+      g.C = B0; g.c_rs = n2; g.c_cs = 1; g.D = it.D;
+      steps[2].push_back(g);
+      g = mk(n0, n12, n0, 1);  // mode 0 back
+      g.A = it.T[0]; g.a_rs = n0; g.a_cs = 1;
+      g.B = B0; g.b_rs = n12; g.b_cs = 1;
+      g.C = B1; g.c_rs = n12; g.c_cs = 1;
+      steps[3].push_back(g);
+      g = mk(n1, n2, n1, n0);  // mode 1 back, batched
+      g.A = it.T[1]; g.a_rs = n1; g.a_cs = 1; g.a_bs = 0;
+      g.B = B1; g.b_rs = n2; g.b_cs = 1; g.b_bs = n12;
+      g.C = B0; g.c_rs = n2; g.c_cs = 1; g.c_bs = n12;
+      steps[4].push_back(g);
+      g = mk(n01, n2, n2, 1);  // mode 2 back -> scatter
+      g.A = B0; g.a_rs = n2; g.a_cs = 1;
+      g.B = it.T[2]; g.b_rs = 1; g.b_cs = n2;
+      g.c_idx = it.idx; g.c_rs = n2; g.c_cs = 1;
+      steps[5].push_back(g);
+    }
+    base += (size_t)n0 * n1 * n2;
+  }
+  for (int s = 0; s < F.nsteps; ++s) {
+    int tb = 0;
+    double bytes = 0;
+    for (auto& g : steps[s]) {
+      g.tiles_m = (g.M + 63) / 64;
+      g.tiles_n = (g.N + 63) / 64;
+      g.tile_base = tb;
+      tb += g.tiles_m * g.tiles_n * g.nb;
+      bytes += 8.0 * g.nb * ((double)g.M * g.N * 2.0) + 8.0 * (double)g.M * g.K;
+      if (g.b_idx) bytes += 4.0 * g.K * (double)g.N;
+      if (g.c_idx) bytes += 4.0 * g.M * (double)g.N + 8.0 * g.M * (double)g.N;
+    }
+    F.ndesc[s] = (int)steps[s].size();
+    F.tiles[s] = tb;
+    F.bytes[s] = bytes;
+    F.d_desc[s] = ctx->upload(steps[s].data(), steps[s].size());
+  }
+}
+
+}  // namespace
+
+// ============================================================================ C ABI
+extern "C" {
+
+int igb_version(void) { return 1; }
+
+int igb_create(igb_ctx** out, int device) {
+  if (!out) return IGB_ERR_ARG;
+  *out = nullptr;
+  igb_ctx* ctx = new (std::nothrow) igb_ctx();
+  if (!ctx) return IGB_ERR_NOMEM;
+  int rc = guarded(ctx, [&] {
+    int count = 0;
+    CU(cudaGetDeviceCount(&count));
+    if (device < 0 || device >= count) throw ArgError("no such CUDA device");
+    ctx->device = device;
+    CU(cudaSetDevice(device));
+    CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CU(cudaEventCreate(&ctx->t0));
+    CU(cudaEventCreate(&ctx->t1));
+    CU(cudaMallocHost(&ctx->sc_host, sizeof(CgScalars)));
+  });
+  if (rc != IGB_OK) {
+    std::fprintf(stderr, "igb_create: %s\n", ctx->err.c_str());
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return IGB_OK;
+}
+
+int igb_destroy(igb_ctx* ctx) {
+  if (!ctx) return IGB_OK;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->drop_graph();
+  for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+  for (void* p : ctx->allocs) cudaFree(p);
+  if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+  if (ctx->t0) cudaEventDestroy(ctx->t0);
+  if (ctx->t1) cudaEventDestroy(ctx->t1);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+  return IGB_OK;
+}
+
+const char* igb_last_error(igb_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int igb_set_num_levels(igb_ctx* ctx, int L) {
+  return guarded(ctx, [&] {
+    if (L < 1) throw ArgError("need at least one refinement level (L >= 1)");
+    if (ctx->L >= 0) throw StateError("hierarchy already sized");
+    ctx->L = L;
+    ctx->lev.resize(L + 1);
+    ctx->steps.assign(L + 1, 1);
+  });
+}
+
+int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz, const int* indptr,
+                         const int* indices, const double* data) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    Level& V = ctx->level(level);
+    if (V.n) throw StateError("level matrix already set");
+    if (n < 1) throw ArgError("empty level matrix");
+    if (nnz >= (1LL << 31)) throw ArgError("nnz exceeds int32 indexing");
+    check_csr(n, n, nnz, indptr, indices);
+    V.n = n;
+    V.A = upload_csr(ctx, n, n, nnz, indptr, indices, data);
+    V.h_ptr.assign(indptr, indptr + n + 1);
+    V.h_col.assign(indices, indices + nnz);
+    std::vector<int> dp = diag_positions(n, indptr, indices, data, "A");
+    V.dpos = ctx->upload(dp.data(), dp.size());
+    V.tri_nnz_lower = V.tri_nnz_upper = 0;
+    for (int i = 0; i < n; ++i) {
+      V.tri_nnz_lower += dp[i] - indptr[i];
+      V.tri_nnz_upper += indptr[i + 1] - dp[i] - 1;
+    }
+    V.f = ctx->alloc<double>(n);
+    V.u = ctx->alloc<double>(n);
+    V.r = ctx->alloc<double>(n);
+    V.c = ctx->alloc<double>(n);
+  });
+}
+
+int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long long nnz,
+                         const int* indptr, const int* indices, const double* data) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    if (level < 1 || level > ctx->L) throw ArgError("prolongation level must be in 1..L");
+    Level& V = ctx->lev[level];
+    if (V.has_P) throw StateError("prolongation already set");
+    check_csr(n_fine, n_coarse, nnz, indptr, indices);
+    V.P = upload_csr(ctx, n_fine, n_coarse, nnz, indptr, indices, data);
+    // transpose on the host (CSR of P^T, sorted columns by construction)
+    std::vector<int> tp(n_coarse + 1, 0), ti(nnz);
+    std::vector<double> tv(nnz);
+    for (long long k = 0; k < nnz; ++k) tp[indices[k] + 1]++;
+    for (int j = 0; j < n_coarse; ++j) tp[j + 1] += tp[j];
+    std::vector<int> pos(tp.begin(), tp.end() - 1);
+    for (int i = 0; i < n_fine; ++i)
+      for (int k = indptr[i]; k < indptr[i + 1]; ++k) {
+        const int p = pos[indices[k]]++;
+        ti[p] = i;
+        tv[p] = data[k];
+      }
+    V.PT = upload_csr(ctx, n_coarse, n_fine, nnz, tp.data(), ti.data(), tv.data());
+    V.has_P = true;
+  });
+}
+
+int igb_set_gs(igb_ctx* ctx, int level) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    Level& V = ctx->level(level);
+    if (!V.n) throw StateError("set the level matrix before igb_set_gs");
+    std::vector<int> dp = diag_positions(V.n, V.h_ptr.data(), V.h_col.data(), nullptr, "A");
+    V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);
+    V.bwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, true);
+    V.has_gs = true;
+  });
+}
+
+int igb_scms_begin(igb_ctx* ctx, int level, double tau) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    Level& V = ctx->level(level);
+    if (!(tau > 0)) throw ArgError("scms needs positive damping");
+    V.has_scms = true;
+    V.tau = tau;
+  });
+}
+
+int igb_scms_add_interior(igb_ctx* ctx, int level, int dim, const int* dims, const double* T0,
+                          const double* T1, const double* T2, const double* denom,
+                          const int* idx) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    Level& V = ctx->level(level);
+    if (!V.has_scms) throw StateError("igb_scms_begin first");
+    if (dim != 2 && dim != 3) throw ArgError("interior dimension must be 2 or 3");
+    InteriorStage it{};
+    it.dim = dim;
+    size_t total = 1;
+    const double* Ts[3] = {T0, T1, T2};
+    for (int a = 0; a < dim; ++a) {
+      if (dims[a] < 1) throw ArgError("empty interior");
+      it.n[a] = dims[a];
+      total *= dims[a];
+      if (!Ts[a]) throw ArgError("null transform");
+    }
+    if (dim == 2) it.n[2] = 1;
+    auto shared = [&](const double* h, size_t count) -> const double* {
+      auto f = ctx->shared_uploads.find(h);
+      if (f != ctx->shared_uploads.end()) return static_cast<const double*>(f->second);
+      double* d = ctx->upload(h, count);
+      ctx->shared_uploads[h] = d;
+      return d;
+    };
+    for (int a = 0; a < dim; ++a) it.T[a] = shared(Ts[a], (size_t)dims[a] * dims[a]);
+    it.D = shared(denom, total);
+    for (size_t k = 0; k < total; ++k)
+      if (idx[k] < 0 || idx[k] >= V.n) throw ArgError("interior index out of range");
+    it.idx = ctx->upload(idx, total);
+    V.interiors.push_back(it);
+  });
+}
+
+int igb_scms_add_piece(igb_ctx* ctx, int level, int m, const int* idx, const double* inv) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    Level& V = ctx->level(level);
+    if (!V.has_scms) throw StateError("igb_scms_begin first");
+    if (m < 1) throw ArgError("empty piece");
+    for (int k = 0; k < m; ++k)
+      if (idx[k] < 0 || idx[k] >= V.n) throw ArgError("piece index out of range");
+    const int* didx = ctx->upload(idx, (size_t)m);
+    const double* dinv = ctx->upload(inv, (size_t)m * m);
+    for (int r0 = 0; r0 < m; r0 += 8) {
+      PieceRowBlock b{dinv, didx, m, r0, std::min(8, m - r0)};
+      V.h_blocks.push_back(b);
+    }
+    V.piece_bytes += 8.0 * m * (double)m + 8.0 * m * 3 + 4.0 * m;
+    V.piece_rows += m;
+  });
+}
+
+int igb_set_coarse_lu(igb_ctx* ctx, int n0, long long l_nnz, const int* l_ptr, const int* l_idx,
+                      const double* l_val, long long u_nnz, const int* u_ptr, const int* u_idx,
+                      const double* u_val, const int* perm_r, const int* perm_c) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    Coarse& C = ctx->coarse;
+    if (C.set) throw StateError("coarse factor already set");
+    check_csr(n0, n0, l_nnz, l_ptr, l_idx);
+    check_csr(n0, n0, u_nnz, u_ptr, u_idx);
+    std::vector<int> inv(n0, -1);
+    for (int i = 0; i < n0; ++i) {
+      if (perm_r[i] < 0 || perm_r[i] >= n0 || perm_c[i] < 0 || perm_c[i] >= n0)
+        throw ArgError("permutation out of range");
+      inv[perm_r[i]] = i;
+    }
+    for (int i = 0; i < n0; ++i)
+      if (inv[i] < 0) throw ArgError("perm_r is not a permutation");
+    std::vector<int> ld = diag_positions(n0, l_ptr, l_idx, l_val, "L");
+    std::vector<int> ud = diag_positions(n0, u_ptr, u_idx, u_val, "U");
+    C.n = n0;
+    C.L = upload_csr(ctx, n0, n0, l_nnz, l_ptr, l_idx, l_val);
+    C.U = upload_csr(ctx, n0, n0, u_nnz, u_ptr, u_idx, u_val);
+    C.Ldpos = ctx->upload(ld.data(), ld.size());
+    C.Udpos = ctx->upload(ud.data(), ud.size());
+    C.Ls = build_schedule(ctx, n0, l_ptr, l_idx, ld, false);
+    C.Us = build_schedule(ctx, n0, u_ptr, u_idx, ud, true);
+    C.inv_perm_r = ctx->upload(inv.data(), inv.size());
+    C.perm_c = ctx->upload(perm_c, (size_t)n0);
+    C.y = ctx->alloc<double>(n0);
+    C.w = ctx->alloc<double>(n0);
+    C.set = true;
+  });
+}
+
+int igb_set_cycle(igb_ctx* ctx, int smoother, int mu, const int* steps_per_level) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    if (smoother < 0 || smoother > 2) throw ArgError("unknown smoother kind");
+    if (mu != 1 && mu != 2) throw ArgError("cycle index mu must be 1 (V) or 2 (W)");
+    ctx->smoother = smoother;
+    ctx->mu = mu;
+    if (steps_per_level)
+      for (int l = 0; l <= ctx->L; ++l) {
+        if (steps_per_level[l] < 0) throw ArgError("negative smoothing steps");
+        ctx->steps[l] = steps_per_level[l];
+      }
+    ctx->drop_graph();
+  });
+}
+
+int igb_finalize(igb_ctx* ctx) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    if (ctx->finalized) throw StateError("already finalized");
+    for (int l = 0; l <= ctx->L; ++l)
+      if (!ctx->lev[l].n) throw StateError("level matrix missing");
+    if (!ctx->coarse.set) throw StateError("coarse factor missing");
+    if (ctx->coarse.n != ctx->lev[0].n) throw ArgError("coarse factor size != n_0");
+    for (int l = 1; l <= ctx->L; ++l) {
+      Level& V = ctx->lev[l];
+      if (!V.has_P) throw StateError("prolongation missing");
+      if (V.P.n != V.n || V.P.m != ctx->lev[l - 1].n) throw ArgError("prolongation shape mismatch");
+      const bool need_gs = ctx->smoother != IGB_SMOOTHER_SCMS;
+      const bool need_scms = ctx->smoother != IGB_SMOOTHER_GS;
+      if (need_gs && !V.has_gs) throw StateError("Gauss-Seidel data missing on a level");
+      if (need_scms && !V.has_scms) throw StateError("SCMS data missing on a level");
+      if (V.has_scms) {
+        build_fd_plan(ctx, V);
+        if (!V.h_blocks.empty()) V.d_blocks = ctx->upload(V.h_blocks.data(), V.h_blocks.size());
+        // the pieces must partition 0..n-1 together with the interiors
+      }
+      V.h_col.clear();
+      V.h_col.shrink_to_fit();
+    }
+    const int nL = ctx->lev[ctx->L].n;
+    ctx->x = ctx->alloc<double>(nL);
+    ctx->d = ctx->alloc<double>(nL);
+    ctx->q = ctx->alloc<double>(nL);
+    ctx->b = ctx->alloc<double>(nL);
+    ctx->partials = ctx->alloc<double>(148 * 8);
+    ctx->counter = ctx->alloc<unsigned>(1);
+    CU(cudaMemset(ctx->counter, 0, sizeof(unsigned)));
+    ctx->sc = ctx->alloc<CgScalars>(1);
+    ctx->finalized = true;
+  });
+}
+
+int igb_cycle(igb_ctx* ctx, int level, const double* f, double* u) {
+  return guarded(ctx, [&] {
+    require_final(ctx);
+    CU(cudaSetDevice(ctx->device));
+    if (level < 1 || level > ctx->L) throw ArgError("cycles act on levels >= 1");
+    Level& V = ctx->lev[level];
+    CU(cudaMemcpyAsync(V.f, f, sizeof(double) * V.n, cudaMemcpyHostToDevice, ctx->stream));
+    if (level == ctx->L) ctx->run_finest_cycle();
+    else ctx->cycle(level, V.f, V.u);
+    CU(cudaMemcpyAsync(u, V.u, sizeof(double) * V.n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+    ctx->harvest_graph();
+    if (ctx->prof) ctx->harvest(ctx->direct_recs, true);
+  });
+}
+
+int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out) {
+  return guarded(ctx, [&] {
+    require_final(ctx);
+    CU(cudaSetDevice(ctx->device));
+    cudaStream_t s = ctx->stream;
+    if (op == IGB_OP_COARSE) {
+      Coarse& C = ctx->coarse;
+      Level& V0 = ctx->lev[0];
+      CU(cudaMemcpyAsync(V0.f, in, sizeof(double) * C.n, cudaMemcpyHostToDevice, s));
+      ctx->coarse_solve(V0.f, V0.u);
+      CU(cudaMemcpyAsync(out, V0.u, sizeof(double) * C.n, cudaMemcpyDeviceToHost, s));
+    } else {
+      Level& V = ctx->level(level);
+      const int n = V.n;
+      switch (op) {
+        case IGB_OP_SPMV:
+        case IGB_OP_RESIDUAL: {
+          CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          if (op == IGB_OP_RESIDUAL)
+            CU(cudaMemcpyAsync(V.c, out, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          ctx->spmv(V.A, V.f, op == IGB_OP_RESIDUAL ? V.c : nullptr, V.r, op == IGB_OP_RESIDUAL ? -1 : 0, K_SPMV);
+          CU(cudaMemcpyAsync(out, V.r, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        case IGB_OP_GS_FWD:
+        case IGB_OP_GS_BWD: {
+          if (!V.has_gs) throw StateError("no Gauss-Seidel data on this level");
+          CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          ctx->gs(level, op == IGB_OP_GS_BWD, V.f, V.u, true);
+          CU(cudaMemcpyAsync(out, V.u, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        case IGB_OP_SCMS: {
+          if (!V.has_scms) throw StateError("no SCMS data on this level");
+          CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          ctx->scms(level, V.f, V.u, true);
+          CU(cudaMemcpyAsync(out, V.u, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        case IGB_OP_RESTRICT: {
+          if (level < 1) throw ArgError("restriction needs level >= 1");
+          Level& C = ctx->lev[level - 1];
+          CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          ctx->spmv(V.PT, V.f, nullptr, C.r, 0, K_TRANSFER);
+          CU(cudaMemcpyAsync(out, C.r, sizeof(double) * C.n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        case IGB_OP_PROLONG: {
+          if (level < 1) throw ArgError("prolongation needs level >= 1");
+          Level& C = ctx->lev[level - 1];
+          CU(cudaMemcpyAsync(C.r, in, sizeof(double) * C.n, cudaMemcpyHostToDevice, s));
+          ctx->spmv(V.P, C.r, nullptr, V.r, 0, K_TRANSFER);
+          CU(cudaMemcpyAsync(out, V.r, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        case IGB_OP_CYCLE: {
+          if (level < 1) throw ArgError("cycles act on levels >= 1");
+          CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+          if (level == ctx->L) ctx->run_finest_cycle();
+          else ctx->cycle(level, V.f, V.u);
+          CU(cudaMemcpyAsync(out, V.u, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+          break;
+        }
+        default:
+          throw ArgError("unknown operator");
+      }
+    }
+    CU(cudaStreamSynchronize(s));
+    ctx->harvest_graph();
+    if (ctx->prof) ctx->harvest(ctx->direct_recs, true);
+  });
+}
+
+static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters, double* d_x,
+                     int* its, double* hist, int hist_cap) {
+  if (max_iters < 0) throw ArgError("max_iters must be >= 0");
+  cudaStream_t s = ctx->stream;
+  const int L = ctx->L;
+  Level& F = ctx->lev[L];
+  const int n = F.n;
+  if (ctx->hist_cap < max_iters) {
+    ctx->hist_dev = ctx->alloc<double>(std::max(1, max_iters));
+    ctx->hist_cap = max_iters;
+  }
+  CgScalars init{};
+  init.tol = tol;
+  *ctx->sc_host = init;
+  CU(cudaMemcpyAsync(ctx->sc, ctx->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
+  CU(cudaEventRecord(ctx->t0, s));
+  ctx->launch(K_CG, 16.0 * n, [&] {
+    launch_dot(s, n, d_b, d_b, ctx->partials, ctx->counter, ctx->sc, FIN_NORMB, nullptr);
+  });
+  ctx->launch(K_CG, 8.0 * n, [&] { launch_fill(s, n, d_x, 0.0); });
+  CU(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  *its = 0;
+  int ncycles = 0;
+  if (ctx->sc_host->normb == 0.0) {
+    CU(cudaEventRecord(ctx->t1, s));
+    CU(cudaEventSynchronize(ctx->t1));
+    float ms = 0;
+    CU(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));
+    ctx->last_pcg_ms = ms;
+    ctx->last_cycle_ms = 0;
+    return;
+  }
+  double* r = F.f;   // CG residual doubles as the cycle input
+  double* z = F.u;   // cycle output
+  ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, r, d_b); });
+  ctx->run_finest_cycle();
+  ++ncycles;
+  ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, ctx->d, z); });
+  ctx->launch(K_CG, 16.0 * n, [&] {
+    launch_dot(s, n, r, z, ctx->partials, ctx->counter, ctx->sc, FIN_RZ0, nullptr);
+  });
+  const DevCsr& A = F.A;
+  int it = 0;
+  for (it = 1; it <= max_iters; ++it) {
+    ctx->launch(K_SPMV, 12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n, [&] {
+      launch_spmv_dot(s, n, A.ptr, A.col, A.val, ctx->d, ctx->q, A.group, ctx->partials,
+                      ctx->counter, ctx->sc, ctx->hist_dev);
+    });
+    ctx->launch(K_CG, 56.0 * n, [&] {
+      launch_cg_update(s, n, d_x, r, ctx->d, ctx->q, ctx->partials, ctx->counter, ctx->sc,
+                       ctx->hist_dev);
+    });
+    CU(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    ctx->harvest_graph();
+    if (ctx->prof) ctx->harvest(ctx->direct_recs, true);
+    if (ctx->sc_host->done) break;
+    if (it == max_iters) break;
+    ctx->run_finest_cycle();
+    ++ncycles;
+    ctx->launch(K_CG, 16.0 * n, [&] {
+      launch_dot(s, n, r, z, ctx->partials, ctx->counter, ctx->sc, FIN_BETA, nullptr);
+    });
+    ctx->launch(K_CG, 24.0 * n, [&] { launch_cg_direction(s, n, ctx->d, z, ctx->sc); });
+  }
+  CU(cudaEventRecord(ctx->t1, s));
+  CU(cudaEventSynchronize(ctx->t1));
+  float ms = 0;
+  CU(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));
+  ctx->last_pcg_ms = ms;
+  const int nit = ctx->sc_host->it;
+  *its = ctx->sc_host->done ? nit : max_iters;
+  const int nh = std::min(nit, hist_cap);
+  if (hist && nh > 0) CU(cudaMemcpy(hist, ctx->hist_dev, sizeof(double) * nh, cudaMemcpyDeviceToHost));
+  ctx->last_cycle_ms = 0;
+  (void)ncycles;
+}
+
+int igb_pcg(igb_ctx* ctx, const double* b, double tol, int max_iters, double* x, int* its,
+            double* hist, int hist_cap) {
+  return guarded(ctx, [&] {
+    require_final(ctx);
+    CU(cudaSetDevice(ctx->device));
+    Level& F = ctx->lev[ctx->L];
+    const int n = F.n;
+    // host -> device copy of b and device -> host copy of x
+    CU(cudaMemcpyAsync(ctx->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
+    pcg_core(ctx, ctx->b, tol, max_iters, ctx->x, its, hist, hist_cap);
+    CU(cudaMemcpyAsync(x, ctx->x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters, double* d_x,
+                   int* its, double* hist, int hist_cap) {
+  return guarded(ctx, [&] {
+    require_final(ctx);
+    CU(cudaSetDevice(ctx->device));
+    pcg_core(ctx, d_b, tol, max_iters, d_x, its, hist, hist_cap);
+  });
+}
+
+int igb_device_alloc(igb_ctx* ctx, long long bytes, void** dptr) {
+  return guarded(ctx, [&] {
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaMalloc(dptr, (size_t)bytes));
+  });
+}
+int igb_device_free(igb_ctx* ctx, void* dptr) {
+  return guarded(ctx, [&] { CU(cudaFree(dptr)); });
+}
+int igb_memcpy_h2d(igb_ctx* ctx, void* dst, const void* src, long long bytes) {
+  return guarded(ctx, [&] {
+    CU(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyHostToDevice, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+int igb_memcpy_d2h(igb_ctx* ctx, void* dst, const void* src, long long bytes) {
+  return guarded(ctx, [&] {
+    CU(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToHost, ctx->stream));
+    CU(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+int igb_last_timing(igb_ctx* ctx, double* pcg_ms, double* cycle_ms_avg) {
+  return guarded(ctx, [&] {
+    if (pcg_ms) *pcg_ms = ctx->last_pcg_ms;
+    if (cycle_ms_avg) *cycle_ms_avg = ctx->last_cycle_ms;
+  });
+}
+
+int igb_profile_enable(igb_ctx* ctx, int on) {
+  return guarded(ctx, [&] {
+    ctx->prof = on != 0;
+  });
+}
+int igb_profile_reset(igb_ctx* ctx) {
+  return guarded(ctx, [&] {
+    for (int c = 0; c < K_NCLASS; ++c) {
+      ctx->prof_ms[c] = 0;
+      ctx->prof_n[c] = 0;
+      ctx->prof_bytes[c] = 0;
+    }
+  });
+}
+int igb_profile_get(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes) {
+  return guarded(ctx, [&] {
+    if (cls < 0 || cls >= K_NCLASS) throw ArgError("unknown kernel class");
+    if (ms) *ms = ctx->prof_ms[cls];
+    if (launches) *launches = ctx->prof_n[cls];
+    if (bytes) *bytes = ctx->prof_bytes[cls];
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,422 @@
+// kernels.cu -- sm_100a kernels of the MG-PCG solve phase (fp64, int32 CSR).
+//
+// Design notes (DESIGN.md has the full roofline discussion):
+//  * SpMV: CSR, G lanes per row (G = 4..32 chosen from the mean row length),
+//    fixed xor-shuffle tree -> bitwise run-to-run deterministic.  HBM-bound.
+//  * Triangular sweeps (Gauss-Seidel in the reference's natural order, coarse
+//    LU solves): host-built level sets, one CTA of 1024 threads, warp per row,
+//    one __syncthreads per dependency level.  Latency-bound by the DAG depth.
+//  * Fast diagonalisation: batched 64x64x16 smem-tiled DFMA GEMM with gather
+//    (B operand), divide-by-eigenvalues and scatter-accumulate epilogues so the
+//    four (2-D) / six (3-D) contractions run as 4 / 6 batched launches for all
+//    patch interiors of a level.
+//  * CG: BLAS-1 kernels with last-block deterministic reductions; CG scalars
+//    (alpha, beta, rz, ||b||) never leave the device.
+//  Elementwise updates use explicit __dmul_rn/__dadd_rn so x + a*y rounds
+//  exactly like numpy's two-step evaluation (no FMA contraction).
+#include "kernels.cuh"
+
+namespace igb {
+
+namespace {
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum over the block; result valid in thread 0.  `red` must hold 32 doubles.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  const int nw = blockDim.x >> 5;
+  v = (threadIdx.x < nw) ? red[threadIdx.x] : 0.0;
+  if (w == 0) v = warp_sum(v);
+  return v;
+}
+
+__device__ void apply_finalize(CgScalars* sc, int kind, double sum, double* hist) {
+  switch (kind) {
+    case FIN_NORMB: sc->normb = sqrt(sum); break;
+    case FIN_RZ0: sc->rz = sum; break;
+    case FIN_ALPHA: sc->pAp = sum; sc->alpha = sc->rz / sum; break;
+    case FIN_REL: {
+      sc->rr = sum;
+      const double rel = sqrt(sum) / sc->normb;
+      sc->rel = rel;
+      if (hist) hist[sc->it] = rel;
+      sc->it += 1;
+      if (rel <= sc->tol) sc->done = 1;
+      break;
+    }
+    case FIN_BETA: sc->beta = sum / sc->rz; sc->rz = sum; break;
+  }
+}
+
+// Publish the block partial; the last block to arrive reduces all partials in
+// index order (deterministic for a fixed grid) and applies the finalize step.
+__device__ void finish_reduction(double blocksum, double* partials, unsigned* counter,
+                                 CgScalars* sc, int kind, double* hist) {
+  __shared__ bool last;
+  __shared__ double red2[32];
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = blocksum;
+    __threadfence();
+    const unsigned t = atomicAdd(counter, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += __ldcg(&partials[i]);
+  v = block_sum(v, red2);
+  if (threadIdx.x == 0) {
+    apply_finalize(sc, kind, v, hist);
+    *counter = 0u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CSR SpMV
+template <int G>
+__global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict__ ptr,
+                                                   const int* __restrict__ col,
+                                                   const double* __restrict__ val,
+                                                   const double* __restrict__ x,
+                                                   const double* z, double* y, int sign) {
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int row = (int)(gt / G);
+  const int lane = (int)(gt % G);
+  double s = 0.0;
+  if (row < n) {
+    const int b = __ldg(&ptr[row]), e = __ldg(&ptr[row + 1]);
+    for (int k = b + lane; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&x[__ldg(&col[k])]), s);
+  }
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (row < n && lane == 0) {
+    if (sign == 0) y[row] = s;
+    else if (sign < 0) y[row] = __dsub_rn(z[row], s);
+    else y[row] = __dadd_rn(z[row], s);
+  }
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) spmv_dot_kernel(int n, const int* __restrict__ ptr,
+                                                       const int* __restrict__ col,
+                                                       const double* __restrict__ val,
+                                                       const double* __restrict__ d,
+                                                       double* __restrict__ q, double* partials,
+                                                       unsigned* counter, CgScalars* sc,
+                                                       double* hist) {
+  __shared__ double red[32];
+  if (sc->done) return;
+  const int rows_per_block = blockDim.x / G;
+  const int lane = threadIdx.x % G;
+  double acc = 0.0;
+  for (int base = blockIdx.x * rows_per_block; base < n; base += gridDim.x * rows_per_block) {
+    const int row = base + threadIdx.x / G;
+    double s = 0.0;
+    if (row < n) {
+      const int b = __ldg(&ptr[row]), e = __ldg(&ptr[row + 1]);
+      for (int k = b + lane; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&d[__ldg(&col[k])]), s);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (row < n && lane == 0) {
+      q[row] = s;
+      acc = fma(d[row], s, acc);
+    }
+  }
+  const double bs = block_sum(acc, red);
+  finish_reduction(bs, partials, counter, sc, FIN_ALPHA, hist);
+}
+
+// ---------------------------------------------------------------------------
+// Level-scheduled triangular solve, one CTA.
+__device__ void trsv_phase(const TrsvPhase& P) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  double* x = P.x;
+  for (int l = 0; l < P.nlev; ++l) {
+    const int b = __ldg(&P.lvl_ptr[l]), e = __ldg(&P.lvl_ptr[l + 1]);
+    for (int k = b + warp; k < e; k += nw) {
+      const int i = __ldg(&P.rows[k]);
+      const int dp = __ldg(&P.dpos[i]);
+      const int jb = P.upper ? dp + 1 : __ldg(&P.ptr[i]);
+      const int je = P.upper ? __ldg(&P.ptr[i + 1]) : dp;
+      double s = 0.0;
+      for (int j = jb + lane; j < je; j += 32) s = fma(__ldg(&P.val[j]), x[__ldg(&P.col[j])], s);
+      s = warp_sum(s);
+      if (lane == 0) {
+        const double bi = P.rhs[P.rhs_idx ? __ldg(&P.rhs_idx[i]) : i];
+        const double xi = __ddiv_rn(__dsub_rn(bi, s), __ldg(&P.val[dp]));
+        x[i] = xi;
+        if (P.uacc) P.uacc[i] = __dadd_rn(P.uacc[i], xi);
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(1024) sptrsv_kernel(TrsvPhase a, TrsvPhase b, int has_b,
+                                                      int n_out, const int* __restrict__ out_idx,
+                                                      double* out) {
+  trsv_phase(a);
+  if (has_b) trsv_phase(b);
+  if (out) {
+    const double* src = has_b ? b.x : a.x;
+    for (int i = threadIdx.x; i < n_out; i += blockDim.x) out[i] = src[__ldg(&out_idx[i])];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Batched GEMM for the fast diagonalisation.
+constexpr int FD_BM = 64, FD_BN = 64, FD_BK = 16;
+
+__global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict__ descs,
+                                                      int ndesc, const double* __restrict__ gsrc,
+                                                      double* sdst, double alpha, int accumulate) {
+  __shared__ double As[FD_BK][FD_BM + 1];
+  __shared__ double Bs[FD_BK][FD_BN + 1];
+  const int t = blockIdx.x;
+  int lo = 0, hi = ndesc - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (descs[mid].tile_base <= t) lo = mid; else hi = mid - 1;
+  }
+  const GemmDesc& g = descs[lo];
+  int tt = t - g.tile_base;
+  const int per_batch = g.tiles_m * g.tiles_n;
+  const int bb = tt / per_batch;
+  tt -= bb * per_batch;
+  const int i0 = (tt / g.tiles_n) * FD_BM, j0 = (tt % g.tiles_n) * FD_BN;
+  const int M = g.M, N = g.N, K = g.K;
+  const double* A = g.A + bb * g.a_bs;
+  const long long boff = bb * g.b_bs;
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const bool a_kfast = (g.a_cs == 1);
+  const bool b_jfast = (g.b_cs == 1);
+
+  double acc[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
+
+  for (int k0 = 0; k0 < K; k0 += FD_BK) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int i, k;
+      if (a_kfast) { i = e >> 4; k = e & 15; } else { i = e & 63; k = e >> 6; }
+      const int gi = i0 + i, gk = k0 + k;
+      As[k][i] = (gi < M && gk < K) ? __ldg(&A[gi * g.a_rs + gk * g.a_cs]) : 0.0;
+      int j;
+      if (b_jfast) { j = e & 63; k = e >> 6; } else { k = e & 15; j = e >> 4; }
+      const int gj = j0 + j, gk2 = k0 + k;
+      double bv = 0.0;
+      if (gj < N && gk2 < K) {
+        const long long off = boff + gk2 * g.b_rs + gj * g.b_cs;
+        bv = g.b_idx ? __ldg(&gsrc[__ldg(&g.b_idx[off])]) : __ldg(&g.B[off]);
+      }
+      Bs[k][j] = bv;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < FD_BK; ++k) {
+      double a[4], b[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) a[r] = As[k][ty + 16 * r];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) b[c] = Bs[k][tx + 16 * c];
+#pragma unroll
+      for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    }
+    __syncthreads();
+  }
+  const long long coff = bb * g.c_bs;
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const int gi = i0 + ty + 16 * r;
+    if (gi >= M) continue;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int gj = j0 + tx + 16 * c;
+      if (gj >= N) continue;
+      const long long off = coff + gi * g.c_rs + gj * g.c_cs;
+      double v = acc[r][c];
+      if (g.D) v = __ddiv_rn(v, __ldg(&g.D[off]));
+      if (g.c_idx) {
+        double* dst = sdst + __ldg(&g.c_idx[off]);
+        const double sv = __dmul_rn(alpha, v);
+        *dst = accumulate ? __dadd_rn(*dst, sv) : sv;
+      } else {
+        g.C[off] = v;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Interface pieces: u[idx[i]] (+)= tau * sum_j inv[i][j] r[idx[j]], warp per row.
+__global__ void __launch_bounds__(256) piece_gemv_kernel(const PieceRowBlock* __restrict__ blocks,
+                                                         const double* __restrict__ r, double* u,
+                                                         double tau, int accumulate) {
+  const PieceRowBlock b = blocks[blockIdx.x];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= b.nrows) return;
+  const int i = b.row0 + warp;
+  const double* row = b.inv + (long long)i * b.m;
+  double s = 0.0;
+  for (int j = lane; j < b.m; j += 32) s = fma(__ldg(&row[j]), __ldg(&r[__ldg(&b.idx[j])]), s);
+  s = warp_sum(s);
+  if (lane == 0) {
+    const int gi = __ldg(&b.idx[i]);
+    const double v = __dmul_rn(tau, s);
+    u[gi] = accumulate ? __dadd_rn(u[gi], v) : v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CG vector kernels
+__global__ void __launch_bounds__(256) dot_kernel(int n, const double* __restrict__ a,
+                                                  const double* __restrict__ b, double* partials,
+                                                  unsigned* counter, CgScalars* sc, int kind,
+                                                  double* hist) {
+  __shared__ double red[32];
+  if (kind != FIN_NORMB && sc->done) return;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc = fma(a[i], b[i], acc);
+  const double bs = block_sum(acc, red);
+  finish_reduction(bs, partials, counter, sc, kind, hist);
+}
+
+__global__ void __launch_bounds__(256) cg_update_kernel(int n, double* __restrict__ x,
+                                                        double* __restrict__ r,
+                                                        const double* __restrict__ d,
+                                                        const double* __restrict__ q,
+                                                        double* partials, unsigned* counter,
+                                                        CgScalars* sc, double* hist) {
+  __shared__ double red[32];
+  if (sc->done) return;
+  const double alpha = sc->alpha;
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    x[i] = __dadd_rn(x[i], __dmul_rn(alpha, d[i]));
+    const double ri = __dsub_rn(r[i], __dmul_rn(alpha, q[i]));
+    r[i] = ri;
+    acc = fma(ri, ri, acc);
+  }
+  const double bs = block_sum(acc, red);
+  finish_reduction(bs, partials, counter, sc, FIN_REL, hist);
+}
+
+__global__ void __launch_bounds__(256) cg_direction_kernel(int n, double* __restrict__ d,
+                                                           const double* __restrict__ z,
+                                                           const CgScalars* sc) {
+  if (sc->done) return;
+  const double beta = sc->beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    d[i] = __dadd_rn(z[i], __dmul_rn(beta, d[i]));
+}
+
+__global__ void copy_kernel(int n, double* __restrict__ dst, const double* __restrict__ src) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = src[i];
+}
+
+__global__ void fill_kernel(int n, double* __restrict__ dst, double v) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    dst[i] = v;
+}
+
+inline int blocks_for(long long threads, int bs) { return (int)((threads + bs - 1) / bs); }
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+int reduction_grid(int n) {
+  int g = (n + 1023) / 1024;  // >= 4 elements per thread
+  if (g < 1) g = 1;
+  if (g > 148 * 8) g = 148 * 8;
+  return g;
+}
+
+void launch_spmv(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
+                 const double* x, const double* z, double* y, int sign, int group) {
+  if (n <= 0) return;
+  const int bs = 256;
+  const long long threads = (long long)n * group;
+  const int grid = blocks_for(threads, bs);
+  switch (group) {
+    case 4: spmv_kernel<4><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
+    case 8: spmv_kernel<8><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
+    case 16: spmv_kernel<16><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
+    default: spmv_kernel<32><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
+  }
+}
+
+void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
+                     const double* d, double* q, int group, double* partials, unsigned* counter,
+                     CgScalars* sc, double* hist) {
+  const int bs = 256;
+  int grid = reduction_grid(n * group / 4);
+  switch (group) {
+    case 4: spmv_dot_kernel<4><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    case 8: spmv_dot_kernel<8><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    case 16: spmv_dot_kernel<16><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    default: spmv_dot_kernel<32><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+  }
+}
+
+void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b, int n_out,
+                   const int* out_idx, double* out) {
+  TrsvPhase bb = b ? *b : a;
+  sptrsv_kernel<<<1, 1024, 0, s>>>(a, bb, b ? 1 : 0, n_out, out_idx, out);
+}
+
+void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,
+                    const double* gsrc, double* sdst, double alpha, int accumulate) {
+  if (total_tiles <= 0) return;
+  fd_gemm_kernel<<<total_tiles, 256, 0, s>>>(d_descs, ndesc, gsrc, sdst, alpha, accumulate);
+}
+
+void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
+                       const double* r, double* u, double tau, int accumulate) {
+  if (nblocks <= 0) return;
+  piece_gemv_kernel<<<nblocks, 256, 0, s>>>(d_blocks, r, u, tau, accumulate);
+}
+
+void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double* partials,
+                unsigned* counter, CgScalars* sc, int kind, double* hist) {
+  dot_kernel<<<reduction_grid(n), 256, 0, s>>>(n, a, b, partials, counter, sc, kind, hist);
+}
+
+void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double* d,
+                      const double* q, double* partials, unsigned* counter, CgScalars* sc,
+                      double* hist) {
+  cg_update_kernel<<<reduction_grid(n), 256, 0, s>>>(n, x, r, d, q, partials, counter, sc, hist);
+}
+
+void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc) {
+  cg_direction_kernel<<<reduction_grid(n), 256, 0, s>>>(n, d, z, sc);
+}
+
+void launch_copy(cudaStream_t s, int n, double* dst, const double* src) {
+  if (n <= 0) return;
+  copy_kernel<<<reduction_grid(n), 256, 0, s>>>(n, dst, src);
+}
+
+void launch_fill(cudaStream_t s, int n, double* dst, double v) {
+  if (n <= 0) return;
+  fill_kernel<<<reduction_grid(n), 256, 0, s>>>(n, dst, v);
+}
+
+}  // namespace igb

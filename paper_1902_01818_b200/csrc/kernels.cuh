@@ -1,0 +1,100 @@
+// kernels.cuh -- device kernels of the MG-PCG solve phase (sm_100a, fp64).
+//
+// Every kernel here replaces one third-party native routine that the
+// reference's solve phase calls:
+//   spmv_*          scipy csr_matvec / csc_matvec        (A@x, f-A@u, P@e, P.T@r)
+//   sptrsv_levels   SuperLU dgstrs on tril(A) / coarse LU (GS sweeps, coarse solve)
+//   fd_gemm         OpenBLAS dgemm under np.tensordot    (SCMS fast diagonalisation)
+//   piece_gemv      SuperLU dgstrs on interface pieces   (SCMS edge/face/vertex)
+//   cg_*            numpy BLAS-1 in linsolve.cg          (dots, norm, axpy)
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace igb {
+
+// ---- CSR SpMV: y = z + sign * A x  (sign 0: y = A x) -----------------------
+void launch_spmv(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
+                 const double* x, const double* z, double* y, int sign, int group);
+
+// ---- level-scheduled triangular solve, one CTA ---------------------------------
+// Solves rows in level order.  For row i (taken from `rows`):
+//   lower (fwd):  uses entries [ptr[i], dpos[i])      x_i = (b_i - s) / val[dpos[i]]
+//   upper (bwd):  uses entries (dpos[i], ptr[i+1])    x_i = (b_i - s) / val[dpos[i]]
+// b_i = rhs[rhs_idx ? rhs_idx[i] : i].  If uacc: uacc[i] += x_i.
+struct TrsvPhase {
+  int nlev;
+  const int* lvl_ptr;   // nlev+1
+  const int* rows;      // n
+  const int* ptr;       // CSR
+  const int* col;
+  const double* val;
+  const int* dpos;      // diagonal position per row
+  int upper;            // 0 fwd / 1 bwd
+  const double* rhs;
+  const int* rhs_idx;   // nullable gather
+  double* x;            // solution (also read for dependencies)
+  double* uacc;         // nullable: uacc[i] += x_i
+};
+// One or two phases run back to back in one launch (coarse: L then U), then an
+// optional output gather out[i] = x_last[out_idx[i]] for i < n_out.
+void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b,
+                   int n_out, const int* out_idx, double* out);
+
+// ---- batched fp64 GEMM for fast diagonalisation ------------------------------
+struct GemmDesc {
+  int M, N, K, nb;           // nb batches with batch strides
+  long long a_rs, a_cs, a_bs;
+  long long b_rs, b_cs, b_bs;
+  long long c_rs, c_cs, c_bs;
+  const double* A;
+  const double* B;
+  const int* b_idx;          // gather: B(k,j) = gsrc[b_idx[off]] (B unused)
+  double* C;
+  const int* c_idx;          // scatter: sdst[c_idx[off]] (+)= alpha * acc
+  const double* D;           // divide: acc / D[off_c]
+  int tiles_m, tiles_n;
+  int tile_base;             // prefix over descriptors
+};
+// gsrc: gather source for descriptors with b_idx; sdst: scatter target for
+// descriptors with c_idx (u[idx] = (accumulate ? u[idx] : 0) + alpha * acc).
+void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,
+                    const double* gsrc, double* sdst, double alpha, int accumulate);
+
+// ---- interface-piece dense solves (precomputed inverses) ---------------------
+struct PieceRowBlock {
+  const double* inv;   // m x m
+  const int* idx;      // m
+  int m;
+  int row0;            // first row handled by this block
+  int nrows;           // rows in this block (<= warps per block)
+};
+void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
+                       const double* r, double* u, double tau, int accumulate);
+
+// ---- CG vector kernels with deterministic reductions -------------------------
+struct CgScalars {
+  double normb, rz, alpha, beta, rel, tol;
+  int it, done;
+  double pAp, rr;
+};
+enum FinalizeKind { FIN_NORMB = 0, FIN_RZ0 = 1, FIN_ALPHA = 2, FIN_REL = 3, FIN_BETA = 4 };
+
+int reduction_grid(int n);
+// q = A d ; then partial d.q -> alpha = rz / (d.q)
+void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
+                     const double* d, double* q, int group, double* partials,
+                     unsigned* counter, CgScalars* sc, double* hist);
+// dot(a, b) with finalize
+void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double* partials,
+                unsigned* counter, CgScalars* sc, int kind, double* hist);
+// x += alpha d ; r -= alpha q ; rr = r.r -> rel
+void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double* d,
+                      const double* q, double* partials, unsigned* counter, CgScalars* sc,
+                      double* hist);
+// d = z + beta d
+void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc);
+void launch_copy(cudaStream_t s, int n, double* dst, const double* src);
+void launch_fill(cudaStream_t s, int n, double* dst, double v);
+
+}  // namespace igb

@@ -137,6 +137,10 @@ int igb_memcpy_d2h(igb_ctx* ctx, void* dst, const void* src, long long bytes);
  * and the average device time of one cycle in it. */
 int igb_last_timing(igb_ctx* ctx, double* pcg_ms, double* cycle_ms_avg);
 
+/* Kernels launched by the library since the last reset (direct launches plus
+ * kernels replayed from the captured cycle graph); reset != 0 clears the count. */
+int igb_launch_count(igb_ctx* ctx, long long* kernels, int reset);
+
 /* Per-kernel-class accumulated device time (ms) and launch counts since
  * igb_profile_reset; classes: 0 spmv, 1 gs, 2 fd, 3 pieces, 4 transfer,
  * 5 coarse, 6 cg-vector. Enabled by igb_profile_enable(ctx, 1). */

@@ -47,6 +47,7 @@ SIGNATURES = {
     "igb_memcpy_h2d": ([_p, _p, _p, _ll], _i),
     "igb_memcpy_d2h": ([_p, _p, _p, _ll], _i),
     "igb_last_timing": ([_p, ctypes.POINTER(_d), ctypes.POINTER(_d)], _i),
+    "igb_launch_count": ([_p, ctypes.POINTER(_ll), _i], _i),
     "igb_profile_enable": ([_p, _i], _i),
     "igb_profile_reset": ([_p], _i),
     "igb_profile_get": ([_p, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll), ctypes.POINTER(_d)], _i),
@@ -223,6 +224,11 @@ class Context:
         a, b = ctypes.c_double(), ctypes.c_double()
         self._check(self.lib.igb_last_timing(self.h, ctypes.byref(a), ctypes.byref(b)), "igb_last_timing")
         return a.value, b.value
+
+    def launch_count(self, reset=False):
+        n = ctypes.c_longlong()
+        self._check(self.lib.igb_launch_count(self.h, ctypes.byref(n), 1 if reset else 0), "igb_launch_count")
+        return n.value
 
     def profile(self, on=True):
         self._check(self.lib.igb_profile_enable(self.h, 1 if on else 0), "igb_profile_enable")

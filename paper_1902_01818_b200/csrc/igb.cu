@@ -153,6 +153,9 @@ struct igb_ctx {
   bool capturing = false;
   bool graph_prof = false;
 
+  // launch accounting (kernels issued directly + kernels replayed from the graph)
+  long long launches_direct = 0, graph_kernels = 0, graph_replays = 0;
+
   // profiling
   bool prof = false;
   std::vector<ProfRec> direct_recs;
@@ -194,6 +197,7 @@ struct igb_ctx {
   // Launch wrapper: records CUDA events around the launch in profile mode.
   template <class F>
   void launch(int cls, double bytes, F&& f) {
+    if (capturing) ++graph_kernels; else ++launches_direct;
     if (!prof) {
       f();
       return;
@@ -206,9 +210,12 @@ struct igb_ctx {
       r.a = pool_event();
       r.b = pool_event();
     }
-    CU(cudaEventRecord(r.a, stream));
+    // inside stream capture a plain record is only a dependency marker; External
+    // makes it a real event-record node that is timestamped at every replay
+    const unsigned fl = capturing ? cudaEventRecordExternal : 0u;
+    CU(cudaEventRecordWithFlags(r.a, stream, fl));
     f();
-    CU(cudaEventRecord(r.b, stream));
+    CU(cudaEventRecordWithFlags(r.b, stream, fl));
     (capturing ? graph_recs : direct_recs).push_back(r);
   }
   void harvest(std::vector<ProfRec>& recs, bool clear) {
@@ -227,6 +234,7 @@ struct igb_ctx {
   void drop_graph() {
     if (cycle_exec) cudaGraphExecDestroy(cycle_exec);
     cycle_exec = nullptr;
+    graph_kernels = 0;
     for (auto& r : graph_recs) {
       cudaEventDestroy(r.a);
       cudaEventDestroy(r.b);
@@ -382,6 +390,7 @@ struct igb_ctx {
       drop_graph();
       cudaGraph_t g;
       capturing = true;
+      graph_kernels = 0;
       CU(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
       try {
         cycle(L, lev[L].f, lev[L].u);
@@ -397,6 +406,7 @@ struct igb_ctx {
       graph_prof = prof;
     }
     CU(cudaGraphLaunch(cycle_exec, stream));
+    ++graph_replays;
   }
   void harvest_graph() {
     if (prof && !graph_recs.empty()) harvest(graph_recs, false);
@@ -1132,6 +1142,16 @@ int igb_profile_reset(igb_ctx* ctx) {
     }
   });
 }
+int igb_launch_count(igb_ctx* ctx, long long* kernels, int reset) {
+  return guarded(ctx, [&] {
+    if (kernels) *kernels = ctx->launches_direct + ctx->graph_kernels * ctx->graph_replays;
+    if (reset) {
+      ctx->launches_direct = 0;
+      ctx->graph_replays = 0;
+    }
+  });
+}
+
 int igb_profile_get(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes) {
   return guarded(ctx, [&] {
     if (cls < 0 || cls >= K_NCLASS) throw ArgError("unknown kernel class");

@@ -1,0 +1,146 @@
+"""Device parity: every hot-path operator and the whole PCG solve vs the oracle.
+
+Calls go through the C-ABI (libigb.so via ctypes).  Tolerances:
+  * single operators (A@x, P@e, P^T r, GS sweeps, SCMS apply, coarse solve,
+    one cycle): relative 2-norm difference <= 1e-12 (fp64, summation-order noise);
+  * PCG: identical iteration counts; residual history max_i |dh_i| / h_1 <= 1e-10
+    and per entry |dh_i| / h_i <= 1e-8 (1e-10 per entry is at
+    the fp64 floor for late entries); solution ||dx|| / ||x|| <= 1e-10;
+  * against the reference's own golden histories the same bounds apply.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import SMALL_CASES, get_setup, load_golden
+
+pytestmark = pytest.mark.gpu
+
+_solvers = {}
+
+
+def device_solver(cfg, **kw):
+    key = (cfg, tuple(sorted(kw.items())))
+    if key not in _solvers:
+        from paper_1902_01818_b200 import multigrid
+        from oracle.solve import OracleSolver
+        pr, setup, f = get_setup(cfg, **kw)
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+        _solvers[key] = (pr, setup, f, solver, OracleSolver(setup.setup_bundle()))
+    return _solvers[key]
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+OP_CASES = [(c, k) for _, c, k in SMALL_CASES] + [("cfg2", {})]
+
+
+@pytest.mark.parametrize("cfg,kw", OP_CASES)
+def test_operators_match_oracle(cfg, kw):
+    pr, setup, f, solver, orc = device_solver(cfg, **kw)
+    ctx = solver.ctx
+    rng = np.random.default_rng(11)
+    for level in range(1, solver.finest + 1):
+        n = solver.A[level].shape[0]
+        nc = solver.A[level - 1].shape[0]
+        x = rng.standard_normal(n)
+        assert rel(ctx.op("spmv", level, x, n), solver.A[level] @ x) <= 1e-12
+        fres = rng.standard_normal(n)
+        assert rel(ctx.op("residual", level, x, n, out_init=fres), fres - solver.A[level] @ x) <= 1e-12
+        if orc.gs[level] is not None:
+            assert rel(ctx.op("gs_fwd", level, x, n), orc.gs_forward(level, x)) <= 1e-12
+            assert rel(ctx.op("gs_bwd", level, x, n), orc.gs_backward(level, x)) <= 1e-12
+        if orc.scms[level] is not None:
+            assert rel(ctx.op("scms", level, x, n), orc.scms_apply(level, x)) <= 1e-12
+        assert rel(ctx.op("restrict", level, x, nc), solver.P[level].T @ x) <= 1e-12
+        xc = rng.standard_normal(nc)
+        assert rel(ctx.op("prolong", level, xc, n), solver.P[level] @ xc) <= 1e-12
+        assert rel(ctx.op("cycle", level, x, n), orc.cycle(level, x)) <= 1e-11
+    x0 = rng.standard_normal(solver.A[0].shape[0])
+    assert rel(ctx.op("coarse", 0, x0, len(x0)), orc.coarse_solve(x0)) <= 1e-11
+
+
+def _check_history(h, ho, tag):
+    h, ho = np.asarray(h), np.asarray(ho)
+    assert len(h) == len(ho), tag
+    assert np.max(np.abs(h - ho)) / ho[0] <= 1e-10, tag
+    assert np.max(np.abs(h - ho) / ho) <= 1e-8, tag
+
+
+@pytest.mark.parametrize("golden,cfg,kw", SMALL_CASES + [("cfg2", "cfg2", {}), ("cfg3", "cfg3", {})])
+def test_pcg_matches_oracle_and_reference(golden, cfg, kw):
+    pr, setup, f, solver, orc = device_solver(cfg, **kw)
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso and rep.converged
+    _check_history(rep.residuals, histo, "vs oracle")
+    assert rel(rep.x, xo) <= 1e-10
+    g = load_golden(golden)
+    assert rep.iterations == int(g["its"])
+    _check_history(rep.residuals, g["hist"], "vs reference golden")
+    assert rel(rep.x, g["x"]) <= 1e-10
+
+
+def test_linsolve_cg_dropin_and_determinism():
+    from paper_1902_01818_b200 import linsolve
+    pr, setup, f, solver, orc = device_solver("cfg2", levels=3)
+    L = solver.finest
+    calls = []
+    x1, its1, h1 = linsolve.cg(solver.A[L], f, solver.preconditioner(), tol=1e-8, max_iters=500,
+                               callback=lambda it, rel_: calls.append(it))
+    x2, its2, h2 = linsolve.cg(solver.A[L], f, solver.preconditioner(), tol=1e-8, max_iters=500)
+    assert its1 == its2 and h1 == h2 and np.array_equal(x1, x2), "device solve is not bitwise reproducible"
+    assert calls == list(range(1, its1 + 1))
+    xr, itsr, hr = linsolve.cg(solver.A[L], f, solver.preconditioner(), tol=1e-14, max_iters=3)
+    assert itsr == 3 and len(hr) == 3
+
+
+def test_zero_rhs_and_spd_check():
+    pr, setup, f, solver, orc = device_solver("cfg1")
+    rep = solver.solve_pcg(np.zeros_like(f))
+    assert rep.iterations == 0 and rep.residuals == [] and not rep.x.any()
+    solver.check_preconditioner_spd()
+
+
+def test_cycle_linearity_and_symmetry_on_device():
+    pr, setup, f, solver, orc = device_solver("cfg3", levels=2)
+    L = solver.finest
+    rng = np.random.default_rng(5)
+    r, s = rng.standard_normal(solver.n_dofs), rng.standard_normal(solver.n_dofs)
+    Br, Bs = solver.cycle(L, r), solver.cycle(L, s)
+    assert abs(s @ Br - r @ Bs) <= 1e-10 * abs(s @ Br)
+    assert rel(solver.cycle(L, 2.0 * r + 3.0 * s), 2.0 * Br + 3.0 * Bs) <= 1e-12
+
+
+def test_stationary_and_direct_drivers():
+    pr, setup, f, solver, orc = device_solver("cfg2", levels=3)
+    for mode in ("stationary", "direct"):
+        rep = solver.solve(f, mode=mode)
+        assert rep.converged and rep.residuals[-1] <= 1e-8
+        assert np.linalg.norm(solver.A[solver.finest] @ rep.x - f) <= 1e-7 * np.linalg.norm(f)
+
+
+def test_smoother_objects_apply_on_device():
+    pr, setup, f, solver, orc = device_solver("cfg2", levels=2)
+    smo = solver.smoother[2]
+    rng = np.random.default_rng(6)
+    r = rng.standard_normal(solver.A[2].shape[0])
+    assert rel(smo.gs.apply_forward(r), orc.gs_forward(2, r)) <= 1e-12
+    assert rel(smo.scms.apply(r), orc.scms_apply(2, r)) <= 1e-12
+
+
+def test_bad_arguments_are_errors():
+    from paper_1902_01818_b200._lib import Context, IgbError
+    ctx = Context(0)
+    with pytest.raises(IgbError):
+        ctx.set_num_levels(0)
+    ctx.set_num_levels(1)
+    import scipy.sparse
+    bad = scipy.sparse.csr_matrix(np.array([[1.0, 2.0], [0.0, 0.0]]))
+    with pytest.raises(IgbError):
+        ctx.set_level_matrix(1, bad)   # zero diagonal
+    with pytest.raises(IgbError):
+        ctx.finalize()                 # incomplete hierarchy
+    ctx.close()

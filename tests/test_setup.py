@@ -1,0 +1,112 @@
+"""Host setup (assembly, transfers, pieces, FD data) pinned to the reference.
+
+The golden fixtures (tests/golden/*.npz, tools/make_golden.py) were produced by
+running the reference igamg package; the product's own setup must reproduce
+its hierarchy sizes exactly and its operators / right-hand sides to 1e-13.
+When /root/reference is importable (this container) the matrices themselves
+are compared directly as well.
+"""
+
+import os
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import REFERENCE_SRC, SMALL_CASES, get_setup, load_golden
+
+
+@pytest.mark.parametrize("golden,cfg,kw", SMALL_CASES + [("cfg2", "cfg2", {}), ("cfg3", "cfg3", {})])
+def test_setup_fingerprints(golden, cfg, kw):
+    g = load_golden(golden)
+    pr, setup, f = get_setup(cfg, **kw)
+    L = setup.finest
+    assert np.array_equal(g["fp_n"], [setup.A[l].shape[0] for l in range(L + 1)])
+    assert np.array_equal(g["fp_nnz"], [setup.A[l].nnz for l in range(L + 1)])
+    assert np.array_equal(g["fp_p_nnz"], [0] + [setup.P[l].nnz for l in range(1, L + 1)])
+    fro = np.array([np.sqrt((setup.A[l].data ** 2).sum()) for l in range(L + 1)])
+    assert np.allclose(fro, g["fp_fro"], rtol=1e-13, atol=0)
+    v = np.random.default_rng(0).standard_normal(setup.n_dofs)
+    Av = setup.A[L] @ v
+    assert np.abs(Av - g["fp_Av"]).max() <= 1e-13 * np.abs(g["fp_Av"]).max()
+    assert np.abs(f - g["f"]).max() <= 1e-13 * np.abs(g["f"]).max()
+
+
+def test_piece_partition_and_kinds():
+    pr, setup, f = get_setup("cfg2", levels=3)
+    scms = setup.smoother[3].scms
+    deco = scms.decomposition
+    deco.validate_partition()
+    kinds = [p.kind for p in deco.pieces]
+    assert kinds.count("interior") == 4 and kinds.count("edge") == 4 and kinds.count("vertex") == 1
+    pr5, setup5, _ = get_setup("cfg5", levels=1)
+    kinds5 = [p.kind for p in setup5.smoother[1].scms.decomposition.pieces]
+    assert (kinds5.count("interior"), kinds5.count("face"), kinds5.count("edge"), kinds5.count("vertex")) == (8, 12, 6, 1)
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg1", {}), ("cfg2", {"levels": 2}), ("cfg5", {"levels": 1})])
+def test_square_transform_equals_subspace_sum(cfg, kw):
+    """sum_alpha T_a (T_a^T R T_a / D_a) T_a^T == T (T^T R T / D) T^T  (SURVEY 8a a7 identity)."""
+    pr, setup, f = get_setup(cfg, **kw)
+    L = setup.finest
+    smo = setup.smoother[L]
+    scms = getattr(smo, "scms", smo)
+    piece, solver = scms.interiors[0]
+    rng = np.random.default_rng(3)
+    R = rng.standard_normal(solver.dims)
+    ref = np.zeros_like(R)
+    for Ts, denom in solver._subspaces:
+        Y = R
+        for a, T in enumerate(Ts):
+            Y = np.moveaxis(np.tensordot(T.T, Y, axes=(1, a)), 0, a)
+        Y = Y / denom
+        for a, T in enumerate(Ts):
+            Y = np.moveaxis(np.tensordot(T, Y, axes=(1, a)), 0, a)
+        ref += Y
+    Ts, D = solver.square_transforms, solver.denominator
+    Y = R
+    for a, T in enumerate(Ts):
+        Y = np.moveaxis(np.tensordot(T.T, Y, axes=(1, a)), 0, a)
+    Y = Y / D
+    for a, T in enumerate(Ts):
+        Y = np.moveaxis(np.tensordot(T, Y, axes=(1, a)), 0, a)
+    assert np.abs(Y - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_piece_inverse_matches_factorization():
+    pr, setup, f = get_setup("cfg2", levels=2)
+    scms = setup.smoother[2].scms
+    A = setup.A[2].tocsr()
+    for (piece, fact), inv in zip(scms.pieces, scms.piece_inverses):
+        sub = A[piece.indices][:, piece.indices].toarray()
+        assert np.abs(sub @ inv - np.eye(len(piece.indices))).max() <= 1e-10
+
+
+def test_coarse_factor_convention():
+    pr, setup, f = get_setup("cfg3", levels=2)
+    L, U, pr_, pc = setup.coarse_solver.factors()
+    b = np.random.default_rng(5).standard_normal(L.shape[0])
+    import scipy.sparse.linalg as sla
+    y = np.empty_like(b)
+    y[pr_] = b
+    w = sla.spsolve_triangular(U, sla.spsolve_triangular(L, y, lower=True), lower=False)
+    x = w[pc]
+    assert np.linalg.norm(setup.A[0] @ x - b) <= 1e-10 * np.linalg.norm(b)
+    assert np.allclose(L.diagonal(), 1.0)
+
+
+@pytest.mark.skipif(not os.path.isdir(REFERENCE_SRC), reason="reference not present")
+def test_matrices_equal_reference_directly():
+    sys.path.insert(0, REFERENCE_SRC)
+    from igamg import assembly as ra, geometry as rg, multigrid as rm
+    dom = rg.l_shape()
+    hier = ra.build_hierarchy(dom, 3, 2, "dg", coarse_elements=2)
+    rs = rm.MultigridSolver(hier, rm.CycleConfig(smoother="hyb"))
+    from paper_1902_01818_b200 import assembly as ma, geometry as mg, multigrid as mm
+    h2 = ma.build_hierarchy(mg.l_shape(), 3, 2, "dg", coarse_elements=2)
+    ms = mm.MultigridSetup(h2, mm.CycleConfig(smoother="hyb"))
+    for l in range(3):
+        d = abs(rs.A[l] - ms.A[l])
+        assert (d.max() if d.nnz else 0.0) <= 1e-13 * abs(rs.A[l]).max()
+    for l in range(1, 3):
+        assert abs(rs.P[l] - ms.P[l]).nnz == 0

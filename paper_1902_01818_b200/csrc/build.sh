@@ -9,6 +9,6 @@ NVCC="${NVCC:-nvcc}"
 "$NVCC" -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
   -Xcompiler -fPIC -Xcompiler -Wall -shared -I"$ROOT/include" -I"$HERE" \
   ${IGB_NVCC_EXTRA:-} \
-  -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/igb.cu"
+  -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/igb.cu" "$HERE/level_plan.cpp"
 mv "$OUT.tmp" "$OUT"
 echo "built $OUT"

@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include "igb.h"
+#include "level_plan.h"
 #include "kernels.cuh"
 
 using namespace igb;
@@ -78,10 +80,20 @@ struct FdPlan {
   int last_scatter = 0;   // step index with the scatter
 };
 
+struct SweepDev {
+  bool ok = false;
+  LevelArgs args{};
+  int threads = 128;
+  long long entries = 0, steps = 0, levels = 0;
+  double stream_bytes = 0;
+};
+
 struct Level {
   int n = 0;
   DevCsr A;
   std::vector<int> h_ptr, h_col;
+  std::vector<double> h_val;
+  SweepDev sweep[2];   // 0: forward (lower) sweep, 1: backward (upper) sweep
   std::vector<double> h_diag;
   int* dpos = nullptr;
   bool has_P = false;
@@ -109,6 +121,7 @@ struct Level {
 struct Coarse {
   bool set = false;
   int n = 0;
+  CoarseCsc csc{};
   DevCsr L, U;
   int *Ldpos = nullptr, *Udpos = nullptr;
   Sched Ls, Us;
@@ -258,6 +271,32 @@ struct igb_ctx {
   // accumulated into u.
   void gs(int l, bool upper, const double* rhs, double* u, bool u_zero) {
     Level& V = lev[l];
+    SweepDev& C = V.sweep[upper ? 1 : 0];
+    if (C.ok) {
+      LevelArgs a = C.args;
+      a.rhs = rhs;
+      a.x = u_zero ? u : V.c;
+      a.uacc = u_zero ? nullptr : u;
+      const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
+      static long long* dbg = nullptr;
+      static const bool want_dbg = std::getenv("IGB_GS_DEBUG") != nullptr;
+      if (want_dbg && !capturing) {
+        if (!dbg) CU(cudaMalloc(&dbg, 8 * sizeof(long long)));
+        a.dbg = dbg;
+        const char* ab = std::getenv("IGB_GS_ABLATE");
+        a.ablate = ab ? std::atoi(ab) : 0;
+      }
+      launch(K_GS, bytes, [&] { launch_level_sweep(stream, a, C.threads); });
+      if (a.dbg) {
+        long long h[8];
+        CU(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        CU(cudaStreamSynchronize(stream));
+        std::fprintf(stderr, "[gs dbg] level %d dir %d n %d steps %lld: chunk %lld gath %lld wait %lld bar %lld comp %lld (cyc/step)\n",
+                     l, upper ? 1 : 0, V.n, h[0], h[1] / h[0], h[2] / h[0], h[3] / h[0], h[4] / h[0], h[5] / h[0]);
+      }
+      return;
+    }
     TrsvPhase ph{};
     const Sched& S = upper ? V.bwd : V.fwd;
     ph.nlev = S.nlev;
@@ -300,6 +339,16 @@ struct igb_ctx {
   }
 
   void coarse_solve(const double* rhs, double* out) {
+    Coarse& C = coarse;
+    if (C.n > 12000) {  // right-hand side no longer fits in shared memory
+      coarse_solve_levels(rhs, out);
+      return;
+    }
+    const double bytes = 12.0 * (C.L.nnz + C.U.nnz) + 8.0 * (C.L.n + 1) + 40.0 * C.n;
+    launch(K_COARSE, bytes, [&] { launch_coarse_csc(stream, C.csc, rhs, out); });
+  }
+
+  void coarse_solve_levels(const double* rhs, double* out) {
     Coarse& C = coarse;
     TrsvPhase a{}, b{};
     a.nlev = C.Ls.nlev; a.lvl_ptr = C.Ls.lvl_ptr; a.rows = C.Ls.rows;
@@ -701,6 +750,7 @@ int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz, const in
     V.A = upload_csr(ctx, n, n, nnz, indptr, indices, data);
     V.h_ptr.assign(indptr, indptr + n + 1);
     V.h_col.assign(indices, indices + nnz);
+    V.h_val.assign(data, data + nnz);
     std::vector<int> dp = diag_positions(n, indptr, indices, data, "A");
     V.dpos = ctx->upload(dp.data(), dp.size());
     V.tri_nnz_lower = V.tri_nnz_upper = 0;
@@ -708,10 +758,11 @@ int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz, const in
       V.tri_nnz_lower += dp[i] - indptr[i];
       V.tri_nnz_upper += indptr[i + 1] - dp[i] - 1;
     }
-    V.f = ctx->alloc<double>(n);
-    V.u = ctx->alloc<double>(n);
-    V.r = ctx->alloc<double>(n);
-    V.c = ctx->alloc<double>(n);
+    // +2: 16-byte gathers of the chain sweep may read one element past the end
+    V.f = ctx->alloc<double>(n + 2);
+    V.u = ctx->alloc<double>(n + 2);
+    V.r = ctx->alloc<double>(n + 2);
+    V.c = ctx->alloc<double>(n + 2);
   });
 }
 
@@ -750,6 +801,41 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     std::vector<int> dp = diag_positions(V.n, V.h_ptr.data(), V.h_col.data(), nullptr, "A");
     V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);
     V.bwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, true);
+    const char* eng = std::getenv("IGB_GS_ENGINE");
+    const bool want_stream = !(eng && std::string(eng) == "levels");
+    level_prepare();
+    for (int dir = 0; dir < 2 && want_stream; ++dir) {
+      SweepDev& C = V.sweep[dir];
+      // (ring slots, chunk lookahead, gather lookahead, chunk bytes)
+      static const int cand[][4] = {{4096, 3, 2, 24576}, {2048, 3, 2, 24576}, {2048, 2, 2, 16384},
+                                    {1024, 2, 1, 16384}};
+      for (const auto& cd : cand) {
+        LevelPlanHost plan;
+        if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
+                              C.threads, cd[0], cd[1], cd[2], cd[3], plan))
+          continue;
+        LevelArgs& a = C.args;
+        a.nsteps = plan.nsteps;
+        a.nchunks = plan.nchunks;
+        a.TPR = plan.TPR;
+        a.R = plan.R;
+        a.D = plan.D;
+        a.G = plan.G;
+        a.chunk_bytes = plan.chunk_bytes;
+        a.ng_slots = plan.max_ng;
+        a.rows_max = plan.max_rows;
+        a.dbg = nullptr;
+        if (level_smem_bytes(a) > 227u * 1024) continue;
+        a.stream = ctx->upload(plan.stream.data(), plan.stream.size());
+        a.chunk_off = ctx->upload(plan.chunk_off.data(), plan.chunk_off.size());
+        C.entries = plan.entries;
+        C.steps = plan.nsteps;
+        C.levels = plan.nlevels;
+        C.stream_bytes = (double)plan.stream.size();
+        C.ok = true;
+        break;
+      }
+    }
     V.has_gs = true;
   });
 }
@@ -847,6 +933,43 @@ int igb_set_coarse_lu(igb_ctx* ctx, int n0, long long l_nnz, const int* l_ptr, c
     C.Us = build_schedule(ctx, n0, u_ptr, u_idx, ud, true);
     C.inv_perm_r = ctx->upload(inv.data(), inv.size());
     C.perm_c = ctx->upload(perm_c, (size_t)n0);
+    // column-oriented copies: strictly lower L and strictly upper U in CSC, diag(U)
+    auto to_csc = [&](const int* p, const int* ix, const double* v, bool lower,
+                      std::vector<int>& cp, std::vector<int>& ri, std::vector<double>& cv) {
+      cp.assign(n0 + 1, 0);
+      for (int i = 0; i < n0; ++i)
+        for (int k = p[i]; k < p[i + 1]; ++k)
+          if (lower ? ix[k] < i : ix[k] > i) cp[ix[k] + 1]++;
+      for (int j = 0; j < n0; ++j) cp[j + 1] += cp[j];
+      ri.resize(cp[n0]);
+      cv.resize(cp[n0]);
+      std::vector<int> pos(cp.begin(), cp.end() - 1);
+      for (int i = 0; i < n0; ++i)
+        for (int k = p[i]; k < p[i + 1]; ++k)
+          if (lower ? ix[k] < i : ix[k] > i) {
+            const int q = pos[ix[k]]++;
+            ri[q] = i;
+            cv[q] = v[k];
+          }
+    };
+    std::vector<int> lcp, lri, ucp, uri;
+    std::vector<double> lcv, ucv, udg(n0);
+    to_csc(l_ptr, l_idx, l_val, true, lcp, lri, lcv);
+    to_csc(u_ptr, u_idx, u_val, false, ucp, uri, ucv);
+    for (int i = 0; i < n0; ++i) {
+      if (l_val[ld[i]] != 1.0) throw ArgError("L must have a unit diagonal");
+      udg[i] = u_val[ud[i]];
+    }
+    C.csc.n = n0;
+    C.csc.lcp = ctx->upload(lcp.data(), lcp.size());
+    C.csc.lri = ctx->upload(lri.data(), lri.size());
+    C.csc.lv = ctx->upload(lcv.data(), lcv.size());
+    C.csc.ucp = ctx->upload(ucp.data(), ucp.size());
+    C.csc.uri = ctx->upload(uri.data(), uri.size());
+    C.csc.uv = ctx->upload(ucv.data(), ucv.size());
+    C.csc.udiag = ctx->upload(udg.data(), udg.size());
+    C.csc.inv_perm_r = C.inv_perm_r;
+    C.csc.perm_c = C.perm_c;
     C.y = ctx->alloc<double>(n0);
     C.w = ctx->alloc<double>(n0);
     C.set = true;
@@ -893,6 +1016,8 @@ int igb_finalize(igb_ctx* ctx) {
       }
       V.h_col.clear();
       V.h_col.shrink_to_fit();
+      V.h_val.clear();
+      V.h_val.shrink_to_fit();
     }
     const int nL = ctx->lev[ctx->L].n;
     ctx->x = ctx->alloc<double>(nL);

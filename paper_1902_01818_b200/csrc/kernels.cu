@@ -174,6 +174,254 @@ __global__ void __launch_bounds__(1024) sptrsv_kernel(TrsvPhase a, TrsvPhase b, 
 }
 
 // ---------------------------------------------------------------------------
+// PTX helpers: mbarrier + TMA bulk copy (cp.async.bulk) + cp.async gathers.
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned cnt) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(cnt) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "MBW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra MBW_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_n(int n) {
+  switch (n) {
+    case 0: asm volatile("cp.async.wait_group 0;" ::: "memory"); break;
+    case 1: asm volatile("cp.async.wait_group 1;" ::: "memory"); break;
+    case 2: asm volatile("cp.async.wait_group 2;" ::: "memory"); break;
+    case 3: asm volatile("cp.async.wait_group 3;" ::: "memory"); break;
+    default: asm volatile("cp.async.wait_group 4;" ::: "memory"); break;
+  }
+}
+
+
+__device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+// Streamed level-set sweep (one CTA of 128 threads).
+//  * The stream is cut into chunks of consecutive step blocks; thread 0 issues
+//    one TMA bulk copy per chunk, D chunks ahead (mbarrier per stage slot).
+//  * G steps ahead, all threads gather (cp.async) the old x values, rhs and u of
+//    a step into a rotating gather slot (G+2 slots).
+//  * Step t: wait for its gathers, barrier, then each row's TPR threads sum
+//    val * U[src] over K (multiple of 4, <= 16) entries, U = shared [ring |
+//    gather slots], reduce with shuffles; x_r = (b_r - s) / a_rr -> ring, x, u.
+// Buffers are refilled only after the barrier that follows their last reader
+// (D+2 chunk slots, G+2 gather slots), so one barrier per step suffices.  All
+// slot / phase bookkeeping is incremental (no integer division on the path).
+template <int K>
+__device__ __forceinline__ double level_dot(const double* __restrict__ vals, const int* __restrict__ srcs,
+                                            int nta, const double* U) {
+  double v[K];
+  int c[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    v[k] = vals[k * nta];
+    c[k] = srcs[k * nta];
+  }
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < K; ++k) acc[k & 3] = fma(v[k], U[c[k]], acc[k & 3]);
+  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
+}
+
+__global__ void __launch_bounds__(128) level_sweep_kernel(LevelArgs a) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  const int S = a.D + 2, GS = a.G + 2;
+  const int slot_stride = 2 * a.ng_slots + 2 * a.rows_max;  // doubles
+  const int cbytes = a.chunk_bytes;
+  unsigned char* stages = sm;
+  double* U = reinterpret_cast<double*>(sm + (size_t)S * cbytes);  // [ring | gather slots]
+  double* ring = U;
+  double* gbase = U + a.R;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(gbase + (size_t)GS * slot_stride);
+  const int tid = threadIdx.x, NT = blockDim.x;
+  const int TPR = a.TPR, rho = tid / TPR, tau = tid - rho * TPR;
+  const int T = a.nsteps, NC = a.nchunks, D = a.D, G = a.G;
+  const int rmask = a.R - 1;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  for (int i = tid; i < a.R; i += NT) ring[i] = 0.0;
+  __syncthreads();
+
+  // chunk issue cursor (thread 0); the end offset of the next chunk is loaded
+  // one issue ahead so the TMA issue never waits on a global load
+  int iss_c = 0, iss_slot = 0;
+  long long iss_lo = a.chunk_off[0], iss_hi = a.chunk_off[NC > 0 ? 1 : 0];
+  auto issue_next = [&]() {
+    unsigned long long* bar = &bars[iss_slot];
+    const unsigned bytes = (unsigned)(iss_hi - iss_lo);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(stages + (size_t)iss_slot * cbytes, a.stream + iss_lo, bytes, bar);
+    ++iss_c;
+    if (++iss_slot == S) iss_slot = 0;
+    iss_lo = iss_hi;
+    if (iss_c < NC) iss_hi = a.chunk_off[iss_c + 1];
+  };
+  // gather cursor: waits on every chunk once (the compute cursor trails it by G steps)
+  int g_slot = 0, g_par = 0, g_off = 0, g_new = 1, g_gs = 0;
+  auto gather_next = [&]() {
+    if (g_new) {
+      mbar_wait(&bars[g_slot], (unsigned)g_par);
+      g_new = 0;
+    }
+    const unsigned char* blk = stages + (size_t)g_slot * cbytes + g_off;
+    const int* hdr = reinterpret_cast<const int*>(blk);
+    const int K = hdr[0], nrows = hdr[1], ng = hdr[2], bytes = hdr[4], nta = hdr[5], cend = hdr[6];
+    if (!(a.ablate & 2)) {
+      const int rpra = (nrows + 3) & ~3;
+      const int* rows = reinterpret_cast<const int*>(blk + 32);
+      const int* gsrc = reinterpret_cast<const int*>(blk + 32 + 12 * rpra + 12 * K * nta);
+      double* xg = gbase + (size_t)g_gs * slot_stride;
+      double* rg = xg + 2 * a.ng_slots;
+      double* ug = rg + a.rows_max;
+      for (int j = tid; j < ng; j += NT) cp_async16(xg + 2 * j, a.x + (gsrc[j] & ~1));
+      for (int i = tid; i < nrows; i += NT) {
+        const int r = rows[i];
+        cp_async8_ca(rg + i, a.rhs + r);
+        if (a.uacc) cp_async8_ca(ug + i, a.uacc + r);
+      }
+    }
+    if (++g_gs == GS) g_gs = 0;
+    if (cend) {
+      g_off = 0;
+      g_new = 1;
+      if (++g_slot == S) {
+        g_slot = 0;
+        g_par ^= 1;
+      }
+    } else {
+      g_off += bytes;
+    }
+  };
+
+  if (tid == 0)
+    for (int c = 0; c < D && c < NC; ++c) issue_next();
+  for (int t = 0; t < G; ++t) {
+    if (t < T) gather_next();
+    cp_async_commit();
+  }
+  int c_slot = 0, c_off = 0, c_new = 1, c_gs = 0;
+  long long c_iss = 0, c_gath = 0, c_wait = 0, c_bar = 0, c_comp = 0, c0 = 0, c1 = 0;
+  const bool dbg = a.dbg != nullptr && tid == 0;
+  for (int t = 0; t < T; ++t) {
+    if (dbg) c0 = clock64();
+    if (c_new) {  // compute cursor entered a new chunk: refill D chunks ahead
+      if (tid == 0 && iss_c < NC) issue_next();
+      c_new = 0;
+    }
+    if (dbg) { c1 = clock64(); c_iss += c1 - c0; c0 = c1; }
+    if (t + G < T) gather_next();
+    cp_async_commit();
+    if (dbg) { c1 = clock64(); c_gath += c1 - c0; c0 = c1; }
+    cp_async_wait_n(G);
+    if (dbg) { c1 = clock64(); c_wait += c1 - c0; c0 = c1; }
+    __syncthreads();
+    if (dbg) { c1 = clock64(); c_bar += c1 - c0; c0 = c1; }
+    const unsigned char* blk = stages + (size_t)c_slot * cbytes + c_off;
+    const int* hdr = reinterpret_cast<const int*>(blk);
+    const int K = hdr[0], nrows = hdr[1], start_pos = hdr[3], bytes = hdr[4], nta = hdr[5], cend = hdr[6];
+    const int rpra = (nrows + 3) & ~3;
+    const int* rows = reinterpret_cast<const int*>(blk + 32);
+    const double* invd = reinterpret_cast<const double*>(blk + 32 + 4 * rpra);
+    const double* vals = reinterpret_cast<const double*>(blk + 32 + 12 * rpra) + tid;
+    const int* srcs = reinterpret_cast<const int*>(blk + 32 + 12 * rpra + 8 * K * nta) + tid;
+    double s = 0.0;
+    if (tid < nta && !(a.ablate & 1)) {
+      switch (K) {
+        case 0: break;
+        case 4: s = level_dot<4>(vals, srcs, nta, U); break;
+        case 8: s = level_dot<8>(vals, srcs, nta, U); break;
+        case 12: s = level_dot<12>(vals, srcs, nta, U); break;
+        default: s = level_dot<16>(vals, srcs, nta, U); break;
+      }
+    }
+    for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (rho < nrows && tau == 0) {
+      const double* rg = gbase + (size_t)c_gs * slot_stride + 2 * a.ng_slots;
+      const double* ug = rg + a.rows_max;
+      const int row = rows[rho];
+      const double xi = __dmul_rn(__dsub_rn(rg[rho], s), invd[rho]);
+      ring[(start_pos + rho) & rmask] = xi;
+      if (!(a.ablate & 4)) {
+        a.x[row] = xi;
+        if (a.uacc) a.uacc[row] = __dadd_rn(ug[rho], xi);
+      }
+    }
+    if (++c_gs == GS) c_gs = 0;
+    if (cend) {
+      c_off = 0;
+      c_new = 1;
+      if (++c_slot == S) c_slot = 0;
+    } else {
+      c_off += bytes;
+    }
+    if (dbg) { c1 = clock64(); c_comp += c1 - c0; }
+  }
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  if (dbg) {
+    a.dbg[0] = T; a.dbg[1] = c_iss; a.dbg[2] = c_gath; a.dbg[3] = c_wait; a.dbg[4] = c_bar; a.dbg[5] = c_comp;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Coarse LU solve, column oriented.
+__global__ void __launch_bounds__(1024) coarse_csc_kernel(CoarseCsc c, const double* __restrict__ rhs,
+                                                          double* __restrict__ out) {
+  extern __shared__ double y[];
+  const int n = c.n;
+  double* w = y + n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = rhs[__ldg(&c.inv_perm_r[i])];
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {  // L y = y, unit diagonal
+    const double yj = y[j];
+    const int b = __ldg(&c.lcp[j]), e = __ldg(&c.lcp[j + 1]);
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+      const int r = __ldg(&c.lri[k]);
+      y[r] = __dsub_rn(y[r], __dmul_rn(__ldg(&c.lv[k]), yj));
+    }
+    __syncthreads();
+  }
+  for (int j = n - 1; j >= 0; --j) {  // U w = y
+    const double wj = __ddiv_rn(y[j], __ldg(&c.udiag[j]));
+    if (threadIdx.x == 0) w[j] = wj;
+    const int b = __ldg(&c.ucp[j]), e = __ldg(&c.ucp[j + 1]);
+    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
+      const int r = __ldg(&c.uri[k]);
+      y[r] = __dsub_rn(y[r], __dmul_rn(__ldg(&c.uv[k]), wj));
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = w[__ldg(&c.perm_c[i])];
+}
+
+// ---------------------------------------------------------------------------
 // Batched GEMM for the fast diagonalisation.
 constexpr int FD_BM = 64, FD_BN = 64, FD_BK = 16;
 
@@ -380,6 +628,35 @@ void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b, int n
                    const int* out_idx, double* out) {
   TrsvPhase bb = b ? *b : a;
   sptrsv_kernel<<<1, 1024, 0, s>>>(a, bb, b ? 1 : 0, n_out, out_idx, out);
+}
+
+void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, double* out) {
+  const size_t smem = 2 * sizeof(double) * (size_t)c.n;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(coarse_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr_set = true;
+  }
+  const int threads = c.n >= 1024 ? 1024 : ((c.n + 31) / 32) * 32;
+  coarse_csc_kernel<<<1, threads < 32 ? 32 : threads, smem, s>>>(c, rhs, out);
+}
+
+size_t level_smem_bytes(const LevelArgs& a) {
+  return (size_t)(a.D + 2) * a.chunk_bytes +
+         8 * ((size_t)a.R + (size_t)(a.G + 2) * (2 * (size_t)a.ng_slots + 2 * (size_t)a.rows_max)) +
+         (size_t)(a.D + 2) * 8;
+}
+
+void level_prepare() {
+  static bool done = false;
+  if (!done) {
+    cudaFuncSetAttribute(level_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    done = true;
+  }
+}
+
+void launch_level_sweep(cudaStream_t s, const LevelArgs& a, int threads) {
+  level_sweep_kernel<<<1, threads, level_smem_bytes(a), s>>>(a);
 }
 
 void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,

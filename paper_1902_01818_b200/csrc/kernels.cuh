@@ -41,6 +41,36 @@ struct TrsvPhase {
 void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b,
                    int n_out, const int* out_idx, double* out);
 
+// ---- streamed level-set triangular sweep (Gauss-Seidel in natural order) ------
+// One CTA; see level_plan.h for the block stream layout.
+struct LevelArgs {
+  const unsigned char* stream;
+  int nsteps, nchunks;
+  const long long* chunk_off;  // nchunks + 1 offsets into the stream
+  const double* rhs;
+  double* x;
+  double* uacc;                // nullable: uacc[r] += x_r
+  int TPR, R, D, G;            // threads per row, ring slots, chunk lookahead, gather lookahead
+  int chunk_bytes, ng_slots, rows_max;
+  long long* dbg;              // nullable: per-phase clock64 totals of thread 0 (debug)
+  int ablate;                  // debug only: bit0 skip entry loop, bit1 skip gathers, bit2 skip stores
+};
+size_t level_smem_bytes(const LevelArgs& a);
+void level_prepare();
+void launch_level_sweep(cudaStream_t s, const LevelArgs& a, int threads);
+
+// ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
+// y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
+// out[i] = w[perm_c[i]].  Column j updates run in parallel; one barrier per column.
+struct CoarseCsc {
+  int n;
+  const int* lcp; const int* lri; const double* lv;   // strictly lower part of L, CSC
+  const int* ucp; const int* uri; const double* uv;   // strictly upper part of U, CSC
+  const double* udiag;                                 // diag of U
+  const int* inv_perm_r; const int* perm_c;
+};
+void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, double* out);
+
 // ---- batched fp64 GEMM for fast diagonalisation ------------------------------
 struct GemmDesc {
   int M, N, K, nb;           // nb batches with batch strides

@@ -83,7 +83,7 @@ struct FdPlan {
 struct SweepDev {
   bool ok = false;
   LevelArgs args{};
-  int threads = 128;
+  int threads = 256;
   long long entries = 0, steps = 0, levels = 0;
   double stream_bytes = 0;
 };

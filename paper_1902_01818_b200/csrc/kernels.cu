@@ -221,7 +221,7 @@ __device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
-// Streamed level-set sweep (one CTA of 128 threads).
+// Streamed level-set sweep (one CTA of 256 threads).
 //  * The stream is cut into chunks of consecutive step blocks; thread 0 issues
 //    one TMA bulk copy per chunk, D chunks ahead (mbarrier per stage slot).
 //  * G steps ahead, all threads gather (cp.async) the old x values, rhs and u of
@@ -248,7 +248,7 @@ __device__ __forceinline__ double level_dot(const double* __restrict__ vals, con
   return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-__global__ void __launch_bounds__(128) level_sweep_kernel(LevelArgs a) {
+__global__ void __launch_bounds__(256) level_sweep_kernel(LevelArgs a) {
   extern __shared__ __align__(128) unsigned char sm[];
   const int S = a.D + 2, GS = a.G + 2;
   const int slot_stride = 2 * a.ng_slots + 2 * a.rows_max;  // doubles

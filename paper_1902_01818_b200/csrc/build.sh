@@ -7,7 +7,7 @@ ROOT="$(dirname "$PKG")"
 OUT="${1:-$PKG/libigb.so}"
 NVCC="${NVCC:-nvcc}"
 "$NVCC" -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
-  -Xcompiler -fPIC -Xcompiler -Wall -shared -I"$ROOT/include" -I"$HERE" \
+  -Xcompiler -fPIC -Xcompiler -Wall -Xlinker --no-undefined -shared -I"$ROOT/include" -I"$HERE" \
   ${IGB_NVCC_EXTRA:-} \
   -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/igb.cu" "$HERE/level_plan.cpp"
 mv "$OUT.tmp" "$OUT"

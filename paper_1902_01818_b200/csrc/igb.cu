@@ -83,7 +83,7 @@ struct FdPlan {
 struct SweepDev {
   bool ok = false;
   LevelArgs args{};
-  int threads = 256;
+  const int* rows = nullptr;   // level order -> row
   long long entries = 0, steps = 0, levels = 0;
   double stream_bytes = 0;
 };
@@ -94,6 +94,8 @@ struct Level {
   std::vector<int> h_ptr, h_col;
   std::vector<double> h_val;
   SweepDev sweep[2];   // 0: forward (lower) sweep, 1: backward (upper) sweep
+  double* rp = nullptr;   // level-ordered right-hand side / solution of the sweep
+  double* xp = nullptr;
   std::vector<double> h_diag;
   int* dpos = nullptr;
   bool has_P = false;
@@ -274,9 +276,8 @@ struct igb_ctx {
     SweepDev& C = V.sweep[upper ? 1 : 0];
     if (C.ok) {
       LevelArgs a = C.args;
-      a.rhs = rhs;
-      a.x = u_zero ? u : V.c;
-      a.uacc = u_zero ? nullptr : u;
+      a.rp = V.rp;
+      a.xp = V.xp;
       const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
       const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
       static long long* dbg = nullptr;
@@ -287,13 +288,16 @@ struct igb_ctx {
         const char* ab = std::getenv("IGB_GS_ABLATE");
         a.ablate = ab ? std::atoi(ab) : 0;
       }
-      launch(K_GS, bytes, [&] { launch_level_sweep(stream, a, C.threads); });
+      launch(K_GS, 20.0 * V.n, [&] { launch_perm_gather(stream, V.n, C.rows, rhs, V.rp); });
+      launch(K_GS, bytes, [&] { launch_level_sweep(stream, a); });
+      launch(K_GS, 20.0 * V.n + (u_zero ? 0.0 : 8.0 * V.n),
+             [&] { launch_perm_scatter(stream, V.n, C.rows, V.xp, u, u_zero ? 0 : 1); });
       if (a.dbg) {
         long long h[8];
         CU(cudaMemcpyAsync(h, dbg, sizeof(h), cudaMemcpyDeviceToHost, stream));
         CU(cudaStreamSynchronize(stream));
-        std::fprintf(stderr, "[gs dbg] level %d dir %d n %d steps %lld: chunk %lld gath %lld wait %lld bar %lld comp %lld (cyc/step)\n",
-                     l, upper ? 1 : 0, V.n, h[0], h[1] / h[0], h[2] / h[0], h[3] / h[0], h[4] / h[0], h[5] / h[0]);
+        std::fprintf(stderr, "[gs dbg] level %d dir %d n %d steps %lld: %lld cyc/step\n", l, upper ? 1 : 0,
+                     V.n, h[0], h[1] / (h[0] > 0 ? h[0] : 1));
       }
       return;
     }
@@ -340,7 +344,7 @@ struct igb_ctx {
 
   void coarse_solve(const double* rhs, double* out) {
     Coarse& C = coarse;
-    if (C.n > 12000) {  // right-hand side no longer fits in shared memory
+    if (C.n > 7000) {  // rhs + column pointers no longer fit in shared memory
       coarse_solve_levels(rhs, out);
       return;
     }
@@ -806,35 +810,41 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     level_prepare();
     for (int dir = 0; dir < 2 && want_stream; ++dir) {
       SweepDev& C = V.sweep[dir];
-      // (ring slots, chunk lookahead, gather lookahead, chunk bytes)
-      static const int cand[][4] = {{4096, 3, 2, 24576}, {2048, 3, 2, 24576}, {2048, 2, 2, 16384},
-                                    {1024, 2, 1, 16384}};
-      for (const auto& cd : cand) {
-        LevelPlanHost plan;
+      LevelPlanHost plan;
+      if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
+                            LEVEL_NT, 16384, LEVEL_KMAX, plan) &&
+          !build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
+                            LEVEL_NT, 4096, LEVEL_KMAX, plan))
+        continue;
+      LevelArgs& a = C.args;
+      a.nsteps = plan.nsteps;
+      a.TPR = plan.TPR;
+      a.R = plan.R;
+      a.dbg = nullptr;
+      a.ablate = 0;
+      if (level_smem_bytes(a) > 220u * 1024) {
         if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
-                              C.threads, cd[0], cd[1], cd[2], cd[3], plan))
+                              LEVEL_NT, 4096, LEVEL_KMAX, plan))
           continue;
-        LevelArgs& a = C.args;
-        a.nsteps = plan.nsteps;
-        a.nchunks = plan.nchunks;
-        a.TPR = plan.TPR;
         a.R = plan.R;
-        a.D = plan.D;
-        a.G = plan.G;
-        a.chunk_bytes = plan.chunk_bytes;
-        a.ng_slots = plan.max_ng;
-        a.rows_max = plan.max_rows;
-        a.dbg = nullptr;
-        if (level_smem_bytes(a) > 227u * 1024) continue;
-        a.stream = ctx->upload(plan.stream.data(), plan.stream.size());
-        a.chunk_off = ctx->upload(plan.chunk_off.data(), plan.chunk_off.size());
-        C.entries = plan.entries;
-        C.steps = plan.nsteps;
-        C.levels = plan.nlevels;
-        C.stream_bytes = (double)plan.stream.size();
-        C.ok = true;
-        break;
+        if (level_smem_bytes(a) > 220u * 1024) continue;
       }
+      static_assert(sizeof(LevelMetaDev) == sizeof(LevelMeta), "meta layout");
+      a.meta = reinterpret_cast<const LevelMetaDev*>(
+          ctx->upload(reinterpret_cast<const int*>(plan.meta.data()), plan.meta.size() * 4));
+      // padded: the sweep prefetches unconditionally past the end of a step / vector
+      plan.stream.resize(plan.stream.size() + 64 * 1024 + 8 * 16 * 32 * 64, 0);
+      a.stream = ctx->upload(plan.stream.data(), plan.stream.size());
+      C.rows = ctx->upload(plan.rows.data(), plan.rows.size());
+      if (!V.rp) {
+        V.rp = ctx->alloc<double>(V.n + LEVEL_NT + 2);
+        V.xp = ctx->alloc<double>(V.n + LEVEL_NT + 2);
+      }
+      C.entries = plan.entries;
+      C.steps = plan.nsteps;
+      C.levels = plan.nlevels;
+      C.stream_bytes = (double)plan.stream.size();
+      C.ok = true;
     }
     V.has_gs = true;
   });
@@ -970,6 +980,8 @@ int igb_set_coarse_lu(igb_ctx* ctx, int n0, long long l_nnz, const int* l_ptr, c
     C.csc.udiag = ctx->upload(udg.data(), udg.size());
     C.csc.inv_perm_r = C.inv_perm_r;
     C.csc.perm_c = C.perm_c;
+    C.csc.lnnz = lcp[n0];
+    C.csc.unnz = ucp[n0];
     C.y = ctx->alloc<double>(n0);
     C.w = ctx->alloc<double>(n0);
     C.set = true;

@@ -221,204 +221,222 @@ __device__ __forceinline__ void cp_async8_ca(void* dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
-// Streamed level-set sweep (one CTA of 256 threads).
-//  * The stream is cut into chunks of consecutive step blocks; thread 0 issues
-//    one TMA bulk copy per chunk, D chunks ahead (mbarrier per stage slot).
-//  * G steps ahead, all threads gather (cp.async) the old x values, rhs and u of
-//    a step into a rotating gather slot (G+2 slots).
-//  * Step t: wait for its gathers, barrier, then each row's TPR threads sum
-//    val * U[src] over K (multiple of 4, <= 16) entries, U = shared [ring |
-//    gather slots], reduce with shuffles; x_r = (b_r - s) / a_rr -> ring, x, u.
-// Buffers are refilled only after the barrier that follows their last reader
-// (D+2 chunk slots, G+2 gather slots), so one barrier per step suffices.  All
-// slot / phase bookkeeping is incremental (no integer division on the path).
-template <int K>
-__device__ __forceinline__ double level_dot(const double* __restrict__ vals, const int* __restrict__ srcs,
-                                            int nta, const double* U) {
-  double v[K];
-  int c[K];
+struct LvlSet {
+  double v[LEVEL_KMAX];
+  int c[LEVEL_KMAX];
+  double b, invd;
+};
+
+template <int KT>
+__device__ __forceinline__ void lvl_load(LvlSet& S, const double2* v2, const int2* c2, long long nthr) {
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    v[k] = vals[k * nta];
-    c[k] = srcs[k * nta];
+  for (int j = 0; j < KT / 2; ++j) {
+    const double2 t = __ldg(v2 + j * nthr);
+    const int2 u = __ldg(c2 + j * nthr);
+    S.v[2 * j] = t.x;
+    S.v[2 * j + 1] = t.y;
+    S.c[2 * j] = u.x;
+    S.c[2 * j + 1] = u.y;
   }
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll
-  for (int k = 0; k < K; ++k) acc[k & 3] = fma(v[k], U[c[k]], acc[k & 3]);
-  return (acc[0] + acc[1]) + (acc[2] + acc[3]);
 }
 
-__global__ void __launch_bounds__(256) level_sweep_kernel(LevelArgs a) {
-  extern __shared__ __align__(128) unsigned char sm[];
-  const int S = a.D + 2, GS = a.G + 2;
-  const int slot_stride = 2 * a.ng_slots + 2 * a.rows_max;  // doubles
-  const int cbytes = a.chunk_bytes;
-  unsigned char* stages = sm;
-  double* U = reinterpret_cast<double*>(sm + (size_t)S * cbytes);  // [ring | gather slots]
-  double* ring = U;
-  double* gbase = U + a.R;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(gbase + (size_t)GS * slot_stride);
-  const int tid = threadIdx.x, NT = blockDim.x;
+template <int KT>
+__device__ __forceinline__ double lvl_dot(const LvlSet& S, const double* ring) {
+  double acc[2] = {0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < KT; ++k) acc[k & 1] = fma(S.v[k], ring[S.c[k]], acc[k & 1]);
+  return acc[0] + acc[1];
+}
+
+// Level-set sweep, one CTA of LEVEL_NT threads, one barrier per step.
+// Thread tid owns row slot rho = tid / TPR and entries tau, tau+TPR, ... of it
+// (kt <= 8 of them), interleaved across threads so that every 128-bit / 64-bit
+// warp load is contiguous.  Four register sets rotate with the step loop
+// unrolled by four: the set of step t+3 is loaded while step t is computed, and
+// nothing reads a loaded register before three steps have passed.  The last
+// thread (idle for small levels) additionally issues a TMA bulk L2 prefetch of
+// block t+PF.  Between two barriers an active thread does kt shared-ring loads,
+// kt FMAs, a TPR-lane shuffle reduction and one store.
+__global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
+  extern __shared__ __align__(16) double lsm[];
+  double* ring = lsm;
+  int4* meta = reinterpret_cast<int4*>(ring + a.R);
+  const int tid = threadIdx.x;
   const int TPR = a.TPR, rho = tid / TPR, tau = tid - rho * TPR;
-  const int T = a.nsteps, NC = a.nchunks, D = a.D, G = a.G;
+  const int T = a.nsteps;
   const int rmask = a.R - 1;
-  if (tid == 0) {
-    for (int s = 0; s < S; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  for (int i = tid; i < a.R; i += NT) ring[i] = 0.0;
+  for (int i = tid; i < a.R; i += LEVEL_NT) ring[i] = 0.0;
+  for (int i = tid; i < T; i += LEVEL_NT) meta[i] = __ldg(reinterpret_cast<const int4*>(a.meta) + i);
   __syncthreads();
 
-  // chunk issue cursor (thread 0); the end offset of the next chunk is loaded
-  // one issue ahead so the TMA issue never waits on a global load
-  int iss_c = 0, iss_slot = 0;
-  long long iss_lo = a.chunk_off[0], iss_hi = a.chunk_off[NC > 0 ? 1 : 0];
-  auto issue_next = [&]() {
-    unsigned long long* bar = &bars[iss_slot];
-    const unsigned bytes = (unsigned)(iss_hi - iss_lo);
-    mbar_expect_tx(bar, bytes);
-    bulk_g2s(stages + (size_t)iss_slot * cbytes, a.stream + iss_lo, bytes, bar);
-    ++iss_c;
-    if (++iss_slot == S) iss_slot = 0;
-    iss_lo = iss_hi;
-    if (iss_c < NC) iss_hi = a.chunk_off[iss_c + 1];
+  auto load = [&](LvlSet& S, int t) {
+    if (t >= T || (a.ablate & 1)) return;
+    const int4 m = meta[t];  // off16, kt | flags, nrows, start
+    const int kt = m.y & 0xffff;
+    const long long nthr = (long long)m.z * TPR;
+    if (tid >= nthr) return;  // a branch, not a select: no load result is consumed here
+    const unsigned char* blk = a.stream + 16LL * m.x;
+    const int rpra = (m.z + 1) & ~1;
+    const double2* v2 = reinterpret_cast<const double2*>(blk + 8 * rpra) + tid;
+    const int2* c2 = reinterpret_cast<const int2*>(blk + 8 * rpra + 8 * kt * nthr) + tid;
+    switch (kt) {
+      case 2: lvl_load<2>(S, v2, c2, nthr); break;
+      case 4: lvl_load<4>(S, v2, c2, nthr); break;
+      case 6: lvl_load<6>(S, v2, c2, nthr); break;
+      default: lvl_load<8>(S, v2, c2, nthr); break;
+    }
+    S.invd = __ldg(reinterpret_cast<const double*>(blk) + rho);
+    S.b = __ldg(a.rp + m.w + rho);
   };
-  // gather cursor: waits on every chunk once (the compute cursor trails it by G steps)
-  int g_slot = 0, g_par = 0, g_off = 0, g_new = 1, g_gs = 0;
-  auto gather_next = [&]() {
-    if (g_new) {
-      mbar_wait(&bars[g_slot], (unsigned)g_par);
-      g_new = 0;
-    }
-    const unsigned char* blk = stages + (size_t)g_slot * cbytes + g_off;
-    const int* hdr = reinterpret_cast<const int*>(blk);
-    const int K = hdr[0], nrows = hdr[1], ng = hdr[2], bytes = hdr[4], nta = hdr[5], cend = hdr[6];
-    if (!(a.ablate & 2)) {
-      const int rpra = (nrows + 3) & ~3;
-      const int* rows = reinterpret_cast<const int*>(blk + 32);
-      const int* gsrc = reinterpret_cast<const int*>(blk + 32 + 12 * rpra + 12 * K * nta);
-      double* xg = gbase + (size_t)g_gs * slot_stride;
-      double* rg = xg + 2 * a.ng_slots;
-      double* ug = rg + a.rows_max;
-      for (int j = tid; j < ng; j += NT) cp_async16(xg + 2 * j, a.x + (gsrc[j] & ~1));
-      for (int i = tid; i < nrows; i += NT) {
-        const int r = rows[i];
-        cp_async8_ca(rg + i, a.rhs + r);
-        if (a.uacc) cp_async8_ca(ug + i, a.uacc + r);
-      }
-    }
-    if (++g_gs == GS) g_gs = 0;
-    if (cend) {
-      g_off = 0;
-      g_new = 1;
-      if (++g_slot == S) {
-        g_slot = 0;
-        g_par ^= 1;
-      }
-    } else {
-      g_off += bytes;
-    }
-  };
-
-  if (tid == 0)
-    for (int c = 0; c < D && c < NC; ++c) issue_next();
-  for (int t = 0; t < G; ++t) {
-    if (t < T) gather_next();
-    cp_async_commit();
-  }
-  int c_slot = 0, c_off = 0, c_new = 1, c_gs = 0;
-  long long c_iss = 0, c_gath = 0, c_wait = 0, c_bar = 0, c_comp = 0, c0 = 0, c1 = 0;
-  const bool dbg = a.dbg != nullptr && tid == 0;
-  for (int t = 0; t < T; ++t) {
-    if (dbg) c0 = clock64();
-    if (c_new) {  // compute cursor entered a new chunk: refill D chunks ahead
-      if (tid == 0 && iss_c < NC) issue_next();
-      c_new = 0;
-    }
-    if (dbg) { c1 = clock64(); c_iss += c1 - c0; c0 = c1; }
-    if (t + G < T) gather_next();
-    cp_async_commit();
-    if (dbg) { c1 = clock64(); c_gath += c1 - c0; c0 = c1; }
-    cp_async_wait_n(G);
-    if (dbg) { c1 = clock64(); c_wait += c1 - c0; c0 = c1; }
-    __syncthreads();
-    if (dbg) { c1 = clock64(); c_bar += c1 - c0; c0 = c1; }
-    const unsigned char* blk = stages + (size_t)c_slot * cbytes + c_off;
-    const int* hdr = reinterpret_cast<const int*>(blk);
-    const int K = hdr[0], nrows = hdr[1], start_pos = hdr[3], bytes = hdr[4], nta = hdr[5], cend = hdr[6];
-    const int rpra = (nrows + 3) & ~3;
-    const int* rows = reinterpret_cast<const int*>(blk + 32);
-    const double* invd = reinterpret_cast<const double*>(blk + 32 + 4 * rpra);
-    const double* vals = reinterpret_cast<const double*>(blk + 32 + 12 * rpra) + tid;
-    const int* srcs = reinterpret_cast<const int*>(blk + 32 + 12 * rpra + 8 * K * nta) + tid;
+  auto compute = [&](const LvlSet& S, int t) {
+    const int4 m = meta[t];
+    const int kt = m.y & 0xffff;
     double s = 0.0;
-    if (tid < nta && !(a.ablate & 1)) {
-      switch (K) {
-        case 0: break;
-        case 4: s = level_dot<4>(vals, srcs, nta, U); break;
-        case 8: s = level_dot<8>(vals, srcs, nta, U); break;
-        case 12: s = level_dot<12>(vals, srcs, nta, U); break;
-        default: s = level_dot<16>(vals, srcs, nta, U); break;
+    if (rho < m.z && !(a.ablate & 2)) {
+      if (m.y >> 16) {  // rare: some entries are old values in global memory
+#pragma unroll
+        for (int k = 0; k < LEVEL_KMAX; ++k) {
+          if (k < kt) {
+            const int c = S.c[k];
+            s = fma(S.v[k], c >= 0 ? ring[c] : a.xp[-c - 1], s);
+          }
+        }
+      } else {
+        switch (kt) {
+          case 2: s = lvl_dot<2>(S, ring); break;
+          case 4: s = lvl_dot<4>(S, ring); break;
+          case 6: s = lvl_dot<6>(S, ring); break;
+          default: s = lvl_dot<8>(S, ring); break;
+        }
       }
     }
+    if (a.ablate & 4) return;
     for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (rho < nrows && tau == 0) {
-      const double* rg = gbase + (size_t)c_gs * slot_stride + 2 * a.ng_slots;
-      const double* ug = rg + a.rows_max;
-      const int row = rows[rho];
-      const double xi = __dmul_rn(__dsub_rn(rg[rho], s), invd[rho]);
-      ring[(start_pos + rho) & rmask] = xi;
-      if (!(a.ablate & 4)) {
-        a.x[row] = xi;
-        if (a.uacc) a.uacc[row] = __dadd_rn(ug[rho], xi);
-      }
+    if (tau == 0 && rho < m.z) {
+      const double xi = __dmul_rn(__dsub_rn(S.b, s), S.invd);
+      ring[(m.w + rho) & rmask] = xi;
+      a.xp[m.w + rho] = xi;
     }
-    if (++c_gs == GS) c_gs = 0;
-    if (cend) {
-      c_off = 0;
-      c_new = 1;
-      if (++c_slot == S) c_slot = 0;
-    } else {
-      c_off += bytes;
+  };
+  constexpr int PF = 10;
+  auto l2_prefetch = [&](int t) {
+    if (tid != LEVEL_NT - 1 || t >= T) return;
+    const int4 m = meta[t];
+    const long long off = 16LL * m.x;
+    const long long end = (t + 1 < T) ? 16LL * meta[t + 1].x : off + 16;
+    if (end > off)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.stream + off), "r"((unsigned)(end - off))
+                   : "memory");
+    const unsigned long long rpa = reinterpret_cast<unsigned long long>(a.rp + m.w) & ~15ULL;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rpa), "r"((unsigned)((8 * m.z + 31) & ~15))
+                 : "memory");
+  };
+  for (int t = 0; t < PF && t < T; ++t) l2_prefetch(t);
+
+  LvlSet A, B, C, D;
+  load(A, 0);
+  load(B, 1);
+  load(C, 2);
+  const long long t_start = clock64();
+  for (int t = 0; t < T; t += 4) {
+    l2_prefetch(t + PF);
+    load(D, t + 3);
+    __syncthreads();
+    compute(A, t);
+    if (t + 1 < T) {
+      l2_prefetch(t + 1 + PF);
+      load(A, t + 4);
+      __syncthreads();
+      compute(B, t + 1);
     }
-    if (dbg) { c1 = clock64(); c_comp += c1 - c0; }
+    if (t + 2 < T) {
+      l2_prefetch(t + 2 + PF);
+      load(B, t + 5);
+      __syncthreads();
+      compute(C, t + 2);
+    }
+    if (t + 3 < T) {
+      l2_prefetch(t + 3 + PF);
+      load(C, t + 6);
+      __syncthreads();
+      compute(D, t + 3);
+    }
   }
-  asm volatile("cp.async.wait_all;" ::: "memory");
-  if (dbg) {
-    a.dbg[0] = T; a.dbg[1] = c_iss; a.dbg[2] = c_gath; a.dbg[3] = c_wait; a.dbg[4] = c_bar; a.dbg[5] = c_comp;
+  if (a.dbg && tid == 0) {
+    a.dbg[0] = T; a.dbg[1] = clock64() - t_start; a.dbg[2] = 0; a.dbg[3] = 0; a.dbg[4] = 0; a.dbg[5] = 0;
+  }
+}
+
+__global__ void perm_gather_kernel(int n, const int* __restrict__ rows, const double* __restrict__ in,
+                                   double* __restrict__ out) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    out[i] = in[__ldg(&rows[i])];
+}
+
+__global__ void perm_scatter_kernel(int n, const int* __restrict__ rows, const double* __restrict__ xp,
+                                    double* __restrict__ u, int accumulate) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int r = __ldg(&rows[i]);
+    u[r] = accumulate ? __dadd_rn(u[r], xp[i]) : xp[i];
   }
 }
 
 // ---------------------------------------------------------------------------
 // Coarse LU solve, column oriented.
+// Column-oriented substitution, one CTA.  The column pointers, and when they
+// fit (RESIDENT) the whole L and U factors, are staged into shared memory
+// first, so a column costs one barrier plus one smem FMA per thread.
+template <bool RESIDENT>
 __global__ void __launch_bounds__(1024) coarse_csc_kernel(CoarseCsc c, const double* __restrict__ rhs,
                                                           double* __restrict__ out) {
   extern __shared__ double y[];
   const int n = c.n;
+  const int NT = blockDim.x, tid = threadIdx.x;
   double* w = y + n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) y[i] = rhs[__ldg(&c.inv_perm_r[i])];
+  double* ud = w + n;
+  double* lv = ud + n;
+  const int lnnz = __ldg(&c.lcp[n]), unnz = __ldg(&c.ucp[n]);
+  double* uv = lv + (RESIDENT ? lnnz : 0);
+  int* lcp = reinterpret_cast<int*>(uv + (RESIDENT ? unnz : 0));
+  int* ucp = lcp + n + 1;
+  int* lri = ucp + n + 1;
+  int* uri = lri + (RESIDENT ? lnnz : 0);
+  for (int i = tid; i < n; i += NT) {
+    y[i] = rhs[__ldg(&c.inv_perm_r[i])];
+    ud[i] = __ldg(&c.udiag[i]);
+  }
+  for (int i = tid; i <= n; i += NT) {
+    lcp[i] = __ldg(&c.lcp[i]);
+    ucp[i] = __ldg(&c.ucp[i]);
+  }
+  const int* Lri = c.lri;
+  const double* Lv = c.lv;
+  const int* Uri = c.uri;
+  const double* Uv = c.uv;
+  if (RESIDENT) {
+    for (int k = tid; k < lnnz; k += NT) { lri[k] = __ldg(&c.lri[k]); lv[k] = __ldg(&c.lv[k]); }
+    for (int k = tid; k < unnz; k += NT) { uri[k] = __ldg(&c.uri[k]); uv[k] = __ldg(&c.uv[k]); }
+    Lri = lri; Lv = lv; Uri = uri; Uv = uv;
+  }
   __syncthreads();
   for (int j = 0; j < n; ++j) {  // L y = y, unit diagonal
     const double yj = y[j];
-    const int b = __ldg(&c.lcp[j]), e = __ldg(&c.lcp[j + 1]);
-    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
-      const int r = __ldg(&c.lri[k]);
-      y[r] = __dsub_rn(y[r], __dmul_rn(__ldg(&c.lv[k]), yj));
+    for (int k = lcp[j] + tid; k < lcp[j + 1]; k += NT) {
+      const int r = Lri[k];
+      y[r] = __dsub_rn(y[r], __dmul_rn(Lv[k], yj));
     }
     __syncthreads();
   }
   for (int j = n - 1; j >= 0; --j) {  // U w = y
-    const double wj = __ddiv_rn(y[j], __ldg(&c.udiag[j]));
-    if (threadIdx.x == 0) w[j] = wj;
-    const int b = __ldg(&c.ucp[j]), e = __ldg(&c.ucp[j + 1]);
-    for (int k = b + threadIdx.x; k < e; k += blockDim.x) {
-      const int r = __ldg(&c.uri[k]);
-      y[r] = __dsub_rn(y[r], __dmul_rn(__ldg(&c.uv[k]), wj));
+    const double wj = __ddiv_rn(y[j], ud[j]);
+    if (tid == 0) w[j] = wj;
+    for (int k = ucp[j] + tid; k < ucp[j + 1]; k += NT) {
+      const int r = Uri[k];
+      y[r] = __dsub_rn(y[r], __dmul_rn(Uv[k], wj));
     }
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = w[__ldg(&c.perm_c[i])];
+  for (int i = tid; i < n; i += NT) out[i] = w[__ldg(&c.perm_c[i])];
 }
 
 // ---------------------------------------------------------------------------
@@ -631,21 +649,22 @@ void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b, int n
 }
 
 void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, double* out) {
-  const size_t smem = 2 * sizeof(double) * (size_t)c.n;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(coarse_csc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(coarse_csc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(coarse_csc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
   const int threads = c.n >= 1024 ? 1024 : ((c.n + 31) / 32) * 32;
-  coarse_csc_kernel<<<1, threads < 32 ? 32 : threads, smem, s>>>(c, rhs, out);
+  const size_t base = 24 * (size_t)c.n + 8 * ((size_t)c.n + 1);
+  const size_t resident = base + 12 * ((size_t)c.lnnz + (size_t)c.unnz);
+  if (resident <= 220 * 1024)
+    coarse_csc_kernel<true><<<1, threads < 32 ? 32 : threads, resident, s>>>(c, rhs, out);
+  else
+    coarse_csc_kernel<false><<<1, threads < 32 ? 32 : threads, base, s>>>(c, rhs, out);
 }
 
-size_t level_smem_bytes(const LevelArgs& a) {
-  return (size_t)(a.D + 2) * a.chunk_bytes +
-         8 * ((size_t)a.R + (size_t)(a.G + 2) * (2 * (size_t)a.ng_slots + 2 * (size_t)a.rows_max)) +
-         (size_t)(a.D + 2) * 8;
-}
+size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R + 16 * (size_t)a.nsteps; }
 
 void level_prepare() {
   static bool done = false;
@@ -655,8 +674,16 @@ void level_prepare() {
   }
 }
 
-void launch_level_sweep(cudaStream_t s, const LevelArgs& a, int threads) {
-  level_sweep_kernel<<<1, threads, level_smem_bytes(a), s>>>(a);
+void launch_level_sweep(cudaStream_t s, const LevelArgs& a) {
+  level_sweep_kernel<<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
+}
+
+void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out) {
+  perm_gather_kernel<<<reduction_grid(n), 256, 0, s>>>(n, rows, in, out);
+}
+
+void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* xp, double* u, int accumulate) {
+  perm_scatter_kernel<<<reduction_grid(n), 256, 0, s>>>(n, rows, xp, u, accumulate);
 }
 
 void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,

@@ -41,23 +41,29 @@ struct TrsvPhase {
 void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b,
                    int n_out, const int* out_idx, double* out);
 
-// ---- streamed level-set triangular sweep (Gauss-Seidel in natural order) ------
-// One CTA; see level_plan.h for the block stream layout.
-struct LevelArgs {
-  const unsigned char* stream;
-  int nsteps, nchunks;
-  const long long* chunk_off;  // nchunks + 1 offsets into the stream
-  const double* rhs;
-  double* x;
-  double* uacc;                // nullable: uacc[r] += x_r
-  int TPR, R, D, G;            // threads per row, ring slots, chunk lookahead, gather lookahead
-  int chunk_bytes, ng_slots, rows_max;
-  long long* dbg;              // nullable: per-phase clock64 totals of thread 0 (debug)
-  int ablate;                  // debug only: bit0 skip entry loop, bit1 skip gathers, bit2 skip stores
+// ---- level-set triangular sweep (Gauss-Seidel in natural order), one CTA ----
+// See level_plan.h: vectors in level order, step metadata staged in shared memory.
+struct LevelMetaDev {
+  int off16, K, nrows, start;
 };
+struct LevelArgs {
+  const LevelMetaDev* meta;
+  int nsteps;
+  const unsigned char* stream;
+  const double* rp;   // right-hand side in level order
+  double* xp;         // solution in level order
+  int TPR, R;
+  long long* dbg;     // nullable: clock64 totals of thread 0 (debug)
+  int ablate;         // debug: bit0 skip loads, bit1 skip dot, bit2 skip reduce+store
+};
+constexpr int LEVEL_NT = 384;
+constexpr int LEVEL_KMAX = 8;
 size_t level_smem_bytes(const LevelArgs& a);
 void level_prepare();
-void launch_level_sweep(cudaStream_t s, const LevelArgs& a, int threads);
+void launch_level_sweep(cudaStream_t s, const LevelArgs& a);
+// out[i] = in[rows[i]]  /  u[rows[i]] (+)= xp[i]
+void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out);
+void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* xp, double* u, int accumulate);
 
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
 // y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
@@ -68,6 +74,7 @@ struct CoarseCsc {
   const int* ucp; const int* uri; const double* uv;   // strictly upper part of U, CSC
   const double* udiag;                                 // diag of U
   const int* inv_perm_r; const int* perm_c;
+  long long lnnz, unnz;                                // host copies of lcp[n], ucp[n]
 };
 void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, double* out);
 

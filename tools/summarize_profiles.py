@@ -1,0 +1,115 @@
+"""Summarise a round's GPU evidence into profiles/ (run here, after gpurun brought files back).
+
+python tools/summarize_profiles.py TAG  (reads gpurun_out/{bench,bench_ref,launches}_TAG.*, prof_*_TAG.ncu-rep)
+Writes profiles/TAG_summary.md, profiles/TAG_launches.csv (per-kernel aggregate of the ncu launch list),
+profiles/TAG_bench.json and the raw ncu metric extracts profiles/TAG_ncu_<kernel>.txt.
+"""
+
+import collections
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+PROF = os.path.join(ROOT, "profiles")
+
+METRICS = [
+    "gpu__time_duration.sum", "sm__cycles_elapsed.max", "dram__bytes_read.sum", "dram__bytes_write.sum",
+    "lts__t_sector_hit_rate.pct", "l1tex__t_sector_hit_rate.pct", "smsp__inst_executed.sum",
+    "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
+    "launch__block_size", "launch__grid_size", "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+    "smsp__sass_thread_inst_executed_op_dfma_pred_on.sum",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+]
+
+
+def last_json(path):
+    with open(path) as fh:
+        for line in reversed(fh.read().strip().splitlines()):
+            if line.startswith("{"):
+                return json.loads(line)
+    return None
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    hi = [i for i, r in enumerate(rows) if r and r[0] == "ID"][0]
+    h = rows[hi]
+    ik, iv = h.index("Kernel Name"), h.index("Metric Value")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= iv:
+            continue
+        name = r[ik].split("(")[0].replace("igb::<unnamed>::", "").replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += float(r[iv].replace(",", ""))
+    return agg
+
+
+def ncu_raw(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    h = rows[0]
+    d = dict(zip(h, rows[2])) if len(rows) > 2 else {}
+    stalls = sorted(((float(v), k.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""))
+                     for k, v in d.items() if k.startswith("smsp__average_warps_issue_stalled")
+                     and k.endswith("per_issue_active.ratio") and v.replace(".", "").isdigit()), reverse=True)
+    return {m: d.get(m) for m in METRICS}, stalls[:8], d.get("Kernel Name", "")
+
+
+def main(tag):
+    os.makedirs(PROF, exist_ok=True)
+    lines = [f"# Round evidence `{tag}`", ""]
+    b = last_json(os.path.join(OUT, f"bench_{tag}.log"))
+    ref = last_json(os.path.join(OUT, f"bench_ref_{tag}.log"))
+    if b:
+        json.dump(b, open(os.path.join(PROF, f"{tag}_bench.json"), "w"), indent=1)
+        lines += ["## bench.py (N=1, cfg2)", "",
+                  f"* value {b['value']:.4g} DoF*it/s, {b['ms_per_step']:.2f} ms per solve, its {b['config']['iterations']}",
+                  f"* e2e {b['e2e']['value']:.4g} DoF*it/s (host buffers)",
+                  f"* cpu_baseline {b['cpu_baseline']['value']:.4g} DoF*it/s ({b['cpu_baseline']['sample']})" if b.get("cpu_baseline") else "",
+                  f"* roofline: dominant class `{b['roofline']['kernel']}`, achieved {b['roofline']['achieved']:.3g} GB/s "
+                  f"= {b['roofline']['frac']:.4f} of measured {b['roofline']['peak']} GB/s",
+                  f"* clocks {b['clocks']}", f"* gpu_launches {b['gpu_launches']}", ""]
+        lines += ["| class | ms / solve | launches / solve | GB/s (algorithmic) |", "|---|---|---|---|"]
+        for k, v in b["roofline"]["classes"].items():
+            lines.append(f"| {k} | {v['ms_per_step']:.3f} | {v['launches_per_step']:.0f} | {v['GBps']:.1f} |")
+        lines.append("")
+    if ref:
+        json.dump(ref, open(os.path.join(PROF, f"{tag}_bench_ref.json"), "w"), indent=1)
+        lines += [f"* reference arm (oracle port, {ref['cpu_baseline']['cores']} threads): {ref['value']:.4g} DoF*it/s, "
+                  f"{ref['ms_per_step']:.1f} ms per solve", ""]
+    lp = os.path.join(OUT, f"launches_{tag}.csv")
+    if os.path.exists(lp):
+        agg = launches(lp)
+        tot = sum(v[1] for v in agg.values())
+        with open(os.path.join(PROF, f"{tag}_launches.csv"), "w") as fh:
+            fh.write("kernel,launches,total_ns,share,avg_us\n")
+            for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+                fh.write(f"{k},{v[0]},{v[1]:.0f},{v[1] / tot:.4f},{v[1] / v[0] / 1e3:.2f}\n")
+        lines += ["## ncu launch list (cold, serialised; shares)", "", "| kernel | launches | share | avg us |",
+                  "|---|---|---|---|"]
+        for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:10]:
+            lines.append(f"| {k} | {v[0]} | {100 * v[1] / tot:.1f}% | {v[1] / v[0] / 1e3:.1f} |")
+        lines.append("")
+    for rep in sorted(f for f in os.listdir(OUT) if f.endswith(f"_{tag}.ncu-rep")):
+        m, stalls, name = ncu_raw(os.path.join(OUT, rep))
+        kname = rep.replace(".ncu-rep", "")
+        with open(os.path.join(PROF, f"{tag}_ncu_{kname}.txt"), "w") as fh:
+            fh.write(f"{name}\n")
+            for k, v in m.items():
+                fh.write(f"{k} = {v}\n")
+            fh.write("stalls (warps per issue-active cycle): " + ", ".join(f"{s}={v:.2f}" for v, s in stalls) + "\n")
+        lines += [f"## ncu --set full: `{kname}`", "", "```"] + [f"{k} = {v}" for k, v in m.items() if v] + [
+            "stalls: " + ", ".join(f"{s}={v:.2f}" for v, s in stalls), "```", ""]
+    with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as fh:
+        fh.write("\n".join(x for x in lines if x is not None) + "\n")
+    print("\n".join(lines))
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "r1b")

@@ -822,11 +822,13 @@ int igb_set_gs(igb_ctx* ctx, int level) {
       a.R = plan.R;
       a.dbg = nullptr;
       a.ablate = 0;
+      a.has_old = plan.has_old ? 1 : 0;
       if (level_smem_bytes(a) > 220u * 1024) {
         if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
                               LEVEL_NT, 4096, LEVEL_KMAX, plan))
           continue;
         a.R = plan.R;
+        a.has_old = plan.has_old ? 1 : 0;
         if (level_smem_bytes(a) > 220u * 1024) continue;
       }
       static_assert(sizeof(LevelMetaDev) == sizeof(LevelMeta), "meta layout");

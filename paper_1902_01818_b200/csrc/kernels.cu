@@ -225,38 +225,19 @@ struct LvlSet {
   double v[LEVEL_KMAX];
   int c[LEVEL_KMAX];
   double b, invd;
+  int nrows, start;
 };
-
-template <int KT>
-__device__ __forceinline__ void lvl_load(LvlSet& S, const double2* v2, const int2* c2, long long nthr) {
-#pragma unroll
-  for (int j = 0; j < KT / 2; ++j) {
-    const double2 t = __ldg(v2 + j * nthr);
-    const int2 u = __ldg(c2 + j * nthr);
-    S.v[2 * j] = t.x;
-    S.v[2 * j + 1] = t.y;
-    S.c[2 * j] = u.x;
-    S.c[2 * j + 1] = u.y;
-  }
-}
-
-template <int KT>
-__device__ __forceinline__ double lvl_dot(const LvlSet& S, const double* ring) {
-  double acc[2] = {0.0, 0.0};
-#pragma unroll
-  for (int k = 0; k < KT; ++k) acc[k & 1] = fma(S.v[k], ring[S.c[k]], acc[k & 1]);
-  return acc[0] + acc[1];
-}
 
 // Level-set sweep, one CTA of LEVEL_NT threads, one barrier per step.
 // Thread tid owns row slot rho = tid / TPR and entries tau, tau+TPR, ... of it
-// (kt <= 8 of them), interleaved across threads so that every 128-bit / 64-bit
-// warp load is contiguous.  Four register sets rotate with the step loop
-// unrolled by four: the set of step t+3 is loaded while step t is computed, and
-// nothing reads a loaded register before three steps have passed.  The last
-// thread (idle for small levels) additionally issues a TMA bulk L2 prefetch of
-// block t+PF.  Between two barriers an active thread does kt shared-ring loads,
-// kt FMAs, a TPR-lane shuffle reduction and one store.
+// (at most LEVEL_KMAX, zero-padded), interleaved across threads so every warp
+// load is contiguous.  Four register sets rotate with the step loop unrolled by
+// four: the set of step t+3 is loaded while step t is computed and nothing reads
+// a loaded register before three steps have passed.  Loads and the dot product
+// are branch-free and fixed-length; OLD (template) adds the rare path for values
+// outside the shared ring (chosen per plan on the host).  The last thread also
+// issues a TMA bulk L2 prefetch of block t+PF.
+template <bool OLD>
 __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   extern __shared__ __align__(16) double lsm[];
   double* ring = lsm;
@@ -270,52 +251,46 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   __syncthreads();
 
   auto load = [&](LvlSet& S, int t) {
-    if (t >= T || (a.ablate & 1)) return;
-    const int4 m = meta[t];  // off16, kt | flags, nrows, start
-    const int kt = m.y & 0xffff;
-    const long long nthr = (long long)m.z * TPR;
+    if (t >= T) return;
+    const int4 m = meta[t];  // off16, kt, nrows, start   (kt == LEVEL_KMAX layout)
+    S.nrows = m.z;
+    S.start = m.w;
+    const int nthr = m.z * TPR;
     if (tid >= nthr) return;  // a branch, not a select: no load result is consumed here
     const unsigned char* blk = a.stream + 16LL * m.x;
     const int rpra = (m.z + 1) & ~1;
     const double2* v2 = reinterpret_cast<const double2*>(blk + 8 * rpra) + tid;
-    const int2* c2 = reinterpret_cast<const int2*>(blk + 8 * rpra + 8 * kt * nthr) + tid;
-    switch (kt) {
-      case 2: lvl_load<2>(S, v2, c2, nthr); break;
-      case 4: lvl_load<4>(S, v2, c2, nthr); break;
-      case 6: lvl_load<6>(S, v2, c2, nthr); break;
-      default: lvl_load<8>(S, v2, c2, nthr); break;
+    const int2* c2 = reinterpret_cast<const int2*>(blk + 8 * rpra + 8 * LEVEL_KMAX * nthr) + tid;
+#pragma unroll
+    for (int j = 0; j < LEVEL_KMAX / 2; ++j) {
+      const double2 vv = __ldg(v2 + j * nthr);
+      const int2 cc = __ldg(c2 + j * nthr);
+      S.v[2 * j] = vv.x;
+      S.v[2 * j + 1] = vv.y;
+      S.c[2 * j] = cc.x;
+      S.c[2 * j + 1] = cc.y;
     }
     S.invd = __ldg(reinterpret_cast<const double*>(blk) + rho);
     S.b = __ldg(a.rp + m.w + rho);
   };
-  auto compute = [&](const LvlSet& S, int t) {
-    const int4 m = meta[t];
-    const int kt = m.y & 0xffff;
-    double s = 0.0;
-    if (rho < m.z && !(a.ablate & 2)) {
-      if (m.y >> 16) {  // rare: some entries are old values in global memory
+  auto compute = [&](const LvlSet& S) {
+    double s0 = 0.0, s1 = 0.0;
+    if (rho < S.nrows) {
 #pragma unroll
-        for (int k = 0; k < LEVEL_KMAX; ++k) {
-          if (k < kt) {
-            const int c = S.c[k];
-            s = fma(S.v[k], c >= 0 ? ring[c] : a.xp[-c - 1], s);
-          }
-        }
-      } else {
-        switch (kt) {
-          case 2: s = lvl_dot<2>(S, ring); break;
-          case 4: s = lvl_dot<4>(S, ring); break;
-          case 6: s = lvl_dot<6>(S, ring); break;
-          default: s = lvl_dot<8>(S, ring); break;
-        }
+      for (int k = 0; k < LEVEL_KMAX; k += 2) {
+        const int c0 = S.c[k], c1 = S.c[k + 1];
+        const double x0 = (OLD && c0 < 0) ? a.xp[-c0 - 1] : ring[OLD ? (c0 < 0 ? 0 : c0) : c0];
+        const double x1 = (OLD && c1 < 0) ? a.xp[-c1 - 1] : ring[OLD ? (c1 < 0 ? 0 : c1) : c1];
+        s0 = fma(S.v[k], x0, s0);
+        s1 = fma(S.v[k + 1], x1, s1);
       }
     }
-    if (a.ablate & 4) return;
+    double s = s0 + s1;
     for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (tau == 0 && rho < m.z) {
+    if (tau == 0 && rho < S.nrows) {
       const double xi = __dmul_rn(__dsub_rn(S.b, s), S.invd);
-      ring[(m.w + rho) & rmask] = xi;
-      a.xp[m.w + rho] = xi;
+      ring[(S.start + rho) & rmask] = xi;
+      a.xp[S.start + rho] = xi;
     }
   };
   constexpr int PF = 10;
@@ -334,6 +309,7 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   for (int t = 0; t < PF && t < T; ++t) l2_prefetch(t);
 
   LvlSet A, B, C, D;
+  A.nrows = B.nrows = C.nrows = D.nrows = 0;
   load(A, 0);
   load(B, 1);
   load(C, 2);
@@ -342,24 +318,24 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
     l2_prefetch(t + PF);
     load(D, t + 3);
     __syncthreads();
-    compute(A, t);
+    compute(A);
     if (t + 1 < T) {
       l2_prefetch(t + 1 + PF);
       load(A, t + 4);
       __syncthreads();
-      compute(B, t + 1);
+      compute(B);
     }
     if (t + 2 < T) {
       l2_prefetch(t + 2 + PF);
       load(B, t + 5);
       __syncthreads();
-      compute(C, t + 2);
+      compute(C);
     }
     if (t + 3 < T) {
       l2_prefetch(t + 3 + PF);
       load(C, t + 6);
       __syncthreads();
-      compute(D, t + 3);
+      compute(D);
     }
   }
   if (a.dbg && tid == 0) {
@@ -669,13 +645,15 @@ size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R + 16 * (siz
 void level_prepare() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(level_sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = true;
   }
 }
 
 void launch_level_sweep(cudaStream_t s, const LevelArgs& a) {
-  level_sweep_kernel<<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
+  if (a.has_old) level_sweep_kernel<true><<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
+  else level_sweep_kernel<false><<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
 }
 
 void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out) {

@@ -53,6 +53,7 @@ struct LevelArgs {
   const double* rp;   // right-hand side in level order
   double* xp;         // solution in level order
   int TPR, R;
+  int has_old;        // some entries read values outside the shared ring
   long long* dbg;     // nullable: clock64 totals of thread 0 (debug)
   int ablate;         // debug: bit0 skip loads, bit1 skip dot, bit2 skip reduce+store
 };

@@ -62,7 +62,8 @@ bool build_level_plan(int n, const int* ptr, const int* col, const double* val, 
         const int r = out.rows[s + i];
         krow = std::max(krow, dep_end(r) - dep_begin(r));
       }
-      const int kt = std::max(2, round_up((krow + TPR - 1) / TPR, 2));
+      const int kt = kmax;  // fixed-length per-thread entry lists (zero padded)
+      (void)krow;
       m.K = kt;
       if (total / 16 >= (1LL << 31)) return false;
       m.off16 = (int)(total / 16);
@@ -107,7 +108,7 @@ bool build_level_plan(int n, const int* ptr, const int* col, const double* val, 
         ++out.entries;
       }
     }
-    if (has_old) m.K |= 1 << 16;  // flag: this step reads old values from global memory
+    if (has_old) out.has_old = true;
     // padding entries stay (0.0, ring slot 0): ring slot 0 always holds a finite value
   }
   return true;

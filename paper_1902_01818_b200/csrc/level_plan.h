@@ -12,8 +12,7 @@
 //
 // Layout (read-only on the device):
 //   meta[t] = {int off16, int K, int nrows, int start}   (block offset in 16-byte units;
-//             K & 0xffff = kt = entries per thread (2, 4, 6 or 8); bit 16 = the
-//             step reads old values from global memory)
+//             K = kt = entries per thread = kmax, zero padded)
 //   block t: [double invd[rpra]] [double2 val[kt/2][nthr]] [int2 src[kt/2][nthr]]
 //     (interleaved so a warp's 128-bit loads are contiguous; nthr = nrows * TPR):
 //     thread i*TPR + j owns row slot i and the row's entries j, j+TPR, ...;
@@ -38,6 +37,7 @@ struct LevelPlanHost {
   int R = 4096;        // ring slots (power of two)
   long long entries = 0;
   long long global_refs = 0;
+  bool has_old = false;        // some entries lie outside the ring
   std::vector<LevelMeta> meta;
   std::vector<int> rows;       // level order -> row
   std::vector<unsigned char> stream;

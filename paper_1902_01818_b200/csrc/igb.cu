@@ -71,6 +71,9 @@ struct InteriorStage {
 };
 
 struct FdPlan {
+  FdSmall* d_small = nullptr;   // fused single-CTA interiors
+  int nsmall = 0, small_nmax = 0;
+  double small_bytes = 0;
   int nsteps = 0;
   GemmDesc* d_desc[6] = {nullptr};
   int ndesc[6] = {0};
@@ -329,6 +332,11 @@ struct igb_ctx {
   void scms(int l, const double* res, double* u, bool u_zero) {
     Level& V = lev[l];
     const FdPlan& F = V.fd;
+    if (F.nsmall) {
+      launch(K_FD, F.small_bytes, [&] {
+        launch_fd_small(stream, F.d_small, F.nsmall, F.small_nmax, res, u, V.tau, u_zero ? 0 : 1);
+      });
+    }
     for (int s = 0; s < F.nsteps; ++s) {
       if (F.ndesc[s] == 0) continue;
       launch(K_FD, F.bytes[s], [&] {
@@ -584,12 +592,30 @@ void require_final(igb_ctx* ctx) {
 
 void build_fd_plan(igb_ctx* ctx, Level& V) {
   if (V.interiors.empty()) return;
-  size_t total = 0;
   int dim = V.interiors[0].dim;
+  // small 2-D interiors: one fused CTA each; the rest: batched GEMM steps
+  std::vector<FdSmall> small;
+  std::vector<InteriorStage> big;
+  const bool fuse = !(std::getenv("IGB_FD_FUSE") && std::string(std::getenv("IGB_FD_FUSE")) == "0");
   for (auto& it : V.interiors) {
     if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
-    total += (size_t)it.n[0] * it.n[1] * (dim == 3 ? it.n[2] : 1);
+    if (fuse && dim == 2 && it.n[0] <= FD_SMALL_NMAX && it.n[1] <= FD_SMALL_NMAX) {
+      FdSmall f{it.T[0], it.T[1], it.D, it.idx, it.n[0], it.n[1]};
+      small.push_back(f);
+      V.fd.small_nmax = std::max(V.fd.small_nmax, std::max(it.n[0], it.n[1]));
+      V.fd.small_bytes += 8.0 * (it.n[0] * it.n[0] + it.n[1] * it.n[1] + 2.0 * it.n[0] * it.n[1]) + 12.0 * it.n[0] * it.n[1];
+    } else {
+      big.push_back(it);
+    }
   }
+  if (!small.empty()) {
+    V.fd.d_small = ctx->upload(small.data(), small.size());
+    V.fd.nsmall = (int)small.size();
+  }
+  V.interiors = big;
+  if (big.empty()) return;
+  size_t total = 0;
+  for (auto& it : V.interiors) total += (size_t)it.n[0] * it.n[1] * (dim == 3 ? it.n[2] : 1);
   V.fd_scratch = total;
   V.s0 = ctx->alloc<double>(total);
   V.s1 = ctx->alloc<double>(total);

@@ -834,40 +834,56 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     const char* eng = std::getenv("IGB_GS_ENGINE");
     const bool want_stream = !(eng && std::string(eng) == "levels");
     level_prepare();
+    const char* clenv = std::getenv("IGB_GS_CLUSTER");
+    const int cluster_max = clenv ? std::max(1, std::min(8, std::atoi(clenv))) : 8;
     for (int dir = 0; dir < 2 && want_stream; ++dir) {
       SweepDev& C = V.sweep[dir];
       LevelPlanHost plan;
-      if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
-                            LEVEL_NT, 16384, LEVEL_KMAX, plan) &&
-          !build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
-                            LEVEL_NT, 4096, LEVEL_KMAX, plan))
-        continue;
       LevelArgs& a = C.args;
-      a.nsteps = plan.nsteps;
-      a.TPR = plan.TPR;
-      a.R = plan.R;
-      a.dbg = nullptr;
-      a.ablate = 0;
-      a.has_old = plan.has_old ? 1 : 0;
-      if (level_smem_bytes(a) > 220u * 1024) {
+      bool ok = false;
+      // steps per level with one CTA decides the cluster size (levels wider than one
+      // CTA's rows go to a cluster), then the largest ring that fits is chosen
+      int ncta = 1;
+      if (cluster_max > 1 &&
+          build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, LEVEL_NT,
+                           4096, LEVEL_KMAX, plan)) {
+        const double per_level = double(plan.nsteps) / std::max(1, plan.nlevels);
+        ncta = std::max(1, std::min(cluster_max, (int)std::ceil(per_level - 1e-9)));
+      }
+      if (const char* force = std::getenv("IGB_GS_FORCE_CLUSTER"))  // testing: cluster even narrow levels
+        ncta = std::max(1, std::min(8, std::atoi(force)));
+      for (int R : {16384, 8192, 4096, 2048}) {
         if (!build_level_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
-                              LEVEL_NT, 4096, LEVEL_KMAX, plan))
+                              LEVEL_NT * ncta, R, LEVEL_KMAX, plan))
           continue;
+        a.nsteps = plan.nsteps;
+        a.TPR = plan.TPR;
         a.R = plan.R;
         a.has_old = plan.has_old ? 1 : 0;
-        if (level_smem_bytes(a) > 220u * 1024) continue;
+        a.cluster = ncta;
+        a.dbg = nullptr;
+        a.ablate = 0;
+        if (level_smem_bytes(a) <= 220u * 1024) {
+          ok = true;
+          break;
+        }
       }
+      if (!ok) continue;
       static_assert(sizeof(LevelMetaDev) == sizeof(LevelMeta), "meta layout");
       a.meta = reinterpret_cast<const LevelMetaDev*>(
           ctx->upload(reinterpret_cast<const int*>(plan.meta.data()), plan.meta.size() * 4));
       // padded: the sweep prefetches unconditionally past the end of a step / vector
-      plan.stream.resize(plan.stream.size() + 64 * 1024 + 8 * 16 * 32 * 64, 0);
+      plan.stream.resize(plan.stream.size() + 64 * 1024 + 8 * 16 * 32 * 64 * 8, 0);
       a.stream = ctx->upload(plan.stream.data(), plan.stream.size());
       C.rows = ctx->upload(plan.rows.data(), plan.rows.size());
       if (!V.rp) {
-        V.rp = ctx->alloc<double>(V.n + LEVEL_NT + 2);
-        V.xp = ctx->alloc<double>(V.n + LEVEL_NT + 2);
+        V.rp = ctx->alloc<double>(V.n + 8 * LEVEL_NT + 2);
+        V.xp = ctx->alloc<double>(V.n + 8 * LEVEL_NT + 2);
       }
+      if (std::getenv("IGB_VERBOSE"))
+        std::fprintf(stderr, "[igb] level %d dir %d: n %d levels %d steps %d TPR %d R %d cluster %d old %d stream %.1f MB\n",
+                     level, dir, V.n, plan.nlevels, plan.nsteps, plan.TPR, plan.R, a.cluster, a.has_old,
+                     plan.stream.size() / 1e6);
       C.entries = plan.entries;
       C.steps = plan.nsteps;
       C.levels = plan.nlevels;

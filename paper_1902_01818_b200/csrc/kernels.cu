@@ -14,7 +14,11 @@
 //    (alpha, beta, rz, ||b||) never leave the device.
 //  Elementwise updates use explicit __dmul_rn/__dadd_rn so x + a*y rounds
 //  exactly like numpy's two-step evaluation (no FMA contraction).
+#include <cooperative_groups.h>
+
 #include "kernels.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace igb {
 
@@ -228,39 +232,60 @@ struct LvlSet {
   int nrows, start;
 };
 
-// Level-set sweep, one CTA of LEVEL_NT threads, one barrier per step.
-// Thread tid owns row slot rho = tid / TPR and entries tau, tau+TPR, ... of it
-// (at most LEVEL_KMAX, zero-padded), interleaved across threads so every warp
-// load is contiguous.  Four register sets rotate with the step loop unrolled by
-// four: the set of step t+3 is loaded while step t is computed and nothing reads
-// a loaded register before three steps have passed.  Loads and the dot product
-// are branch-free and fixed-length; OLD (template) adds the rare path for values
-// outside the shared ring (chosen per plan on the host).  The last thread also
-// issues a TMA bulk L2 prefetch of block t+PF.
-template <bool OLD>
+// Level-set sweep, one CTA (or a cluster of CTAs) of LEVEL_NT threads each, one
+// barrier per step.  Virtual thread vt = cluster_rank * LEVEL_NT + tid owns row
+// slot rho = vt / TPR and entries tau, tau+TPR, ... of it (at most LEVEL_KMAX,
+// zero-padded), interleaved across threads so every warp load is contiguous.
+// Four register sets rotate with the step loop unrolled by four: the set of
+// step t+3 is loaded while step t is computed and nothing reads a loaded
+// register before three steps have passed.  Loads and the dot product are
+// branch-free and fixed-length; OLD adds the rare path for values outside the
+// shared ring.  CLUSTER: every CTA keeps a full copy of the ring; a row's owner
+// writes its value into all CTAs' rings through distributed shared memory and
+// the step barrier is the cluster barrier (release/acquire).  The last thread of
+// each CTA issues a TMA bulk L2 prefetch of block t+PF.
+template <bool OLD, bool CLUSTER>
 __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   extern __shared__ __align__(16) double lsm[];
   double* ring = lsm;
-  int4* meta = reinterpret_cast<int4*>(ring + a.R);
+  const int4* meta = reinterpret_cast<const int4*>(a.meta);  // read-only, L1-cached, used 3 steps ahead
   const int tid = threadIdx.x;
-  const int TPR = a.TPR, rho = tid / TPR, tau = tid - rho * TPR;
+  const int rank = CLUSTER ? (int)cg::this_cluster().block_rank() : 0;
+  const int ncta = CLUSTER ? (int)cg::this_cluster().num_blocks() : 1;
+  const int vt = rank * LEVEL_NT + tid;
+  const int TPR = a.TPR, rho = vt / TPR, tau = vt - rho * TPR;
   const int T = a.nsteps;
   const int rmask = a.R - 1;
   for (int i = tid; i < a.R; i += LEVEL_NT) ring[i] = 0.0;
-  for (int i = tid; i < T; i += LEVEL_NT) meta[i] = __ldg(reinterpret_cast<const int4*>(a.meta) + i);
-  __syncthreads();
+  double* rings[8];
+  if (CLUSTER) {
+    for (int r = 0; r < 8; ++r) rings[r] = r < ncta ? cg::this_cluster().map_shared_rank(ring, r) : ring;
+    cg::this_cluster().sync();
+  } else {
+    __syncthreads();
+  }
+  // CTA: one __syncthreads per step.  Cluster: the barrier is split -- arrive
+  // (release) right after this thread's ring writes, wait (acquire) just before
+  // the next compute -- so its latency overlaps the next step's load issue.
+  auto arrive = [&]() {
+    if (CLUSTER) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  };
+  auto step_barrier = [&]() {
+    if (CLUSTER) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else __syncthreads();
+  };
 
   auto load = [&](LvlSet& S, int t) {
     if (t >= T) return;
-    const int4 m = meta[t];  // off16, kt, nrows, start   (kt == LEVEL_KMAX layout)
+    const int4 m = __ldg(meta + t);  // off16, kt, nrows, start   (kt == LEVEL_KMAX layout)
     S.nrows = m.z;
     S.start = m.w;
     const int nthr = m.z * TPR;
-    if (tid >= nthr) return;  // a branch, not a select: no load result is consumed here
+    if (vt >= nthr) return;  // a branch, not a select: no load result is consumed here
     const unsigned char* blk = a.stream + 16LL * m.x;
     const int rpra = (m.z + 1) & ~1;
-    const double2* v2 = reinterpret_cast<const double2*>(blk + 8 * rpra) + tid;
-    const int2* c2 = reinterpret_cast<const int2*>(blk + 8 * rpra + 8 * LEVEL_KMAX * nthr) + tid;
+    const double2* v2 = reinterpret_cast<const double2*>(blk + 8 * rpra) + vt;
+    const int2* c2 = reinterpret_cast<const int2*>(blk + 8 * rpra + 8 * LEVEL_KMAX * nthr) + vt;
 #pragma unroll
     for (int j = 0; j < LEVEL_KMAX / 2; ++j) {
       const double2 vv = __ldg(v2 + j * nthr);
@@ -289,16 +314,21 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
     for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (tau == 0 && rho < S.nrows) {
       const double xi = __dmul_rn(__dsub_rn(S.b, s), S.invd);
-      ring[(S.start + rho) & rmask] = xi;
+      const int slot = (S.start + rho) & rmask;
+      if (CLUSTER) {
+        for (int r = 0; r < ncta; ++r) rings[r][slot] = xi;
+      } else {
+        ring[slot] = xi;
+      }
       a.xp[S.start + rho] = xi;
     }
   };
   constexpr int PF = 10;
   auto l2_prefetch = [&](int t) {
     if (tid != LEVEL_NT - 1 || t >= T) return;
-    const int4 m = meta[t];
+    const int4 m = __ldg(meta + t);
     const long long off = 16LL * m.x;
-    const long long end = (t + 1 < T) ? 16LL * meta[t + 1].x : off + 16;
+    const long long end = (t + 1 < T) ? 16LL * __ldg(meta + t + 1).x : off + 16;
     if (end > off)
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a.stream + off), "r"((unsigned)(end - off))
                    : "memory");
@@ -314,31 +344,37 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   load(B, 1);
   load(C, 2);
   const long long t_start = clock64();
+  arrive();
   for (int t = 0; t < T; t += 4) {
     l2_prefetch(t + PF);
     load(D, t + 3);
-    __syncthreads();
+    step_barrier();
     compute(A);
+    arrive();
     if (t + 1 < T) {
       l2_prefetch(t + 1 + PF);
       load(A, t + 4);
-      __syncthreads();
+      step_barrier();
       compute(B);
+      arrive();
     }
     if (t + 2 < T) {
       l2_prefetch(t + 2 + PF);
       load(B, t + 5);
-      __syncthreads();
+      step_barrier();
       compute(C);
+      arrive();
     }
     if (t + 3 < T) {
       l2_prefetch(t + 3 + PF);
       load(C, t + 6);
-      __syncthreads();
+      step_barrier();
       compute(D);
+      arrive();
     }
   }
-  if (a.dbg && tid == 0) {
+  step_barrier();  // matches the last arrive; no CTA exits while peers still write into its ring
+  if (a.dbg && tid == 0 && rank == 0) {
     a.dbg[0] = T; a.dbg[1] = clock64() - t_start; a.dbg[2] = 0; a.dbg[3] = 0; a.dbg[4] = 0; a.dbg[5] = 0;
   }
 }
@@ -737,20 +773,40 @@ void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, do
     coarse_csc_kernel<false><<<1, threads < 32 ? 32 : threads, base, s>>>(c, rhs, out);
 }
 
-size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R + 16 * (size_t)a.nsteps; }
+size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }
 
 void level_prepare() {
   static bool done = false;
   if (!done) {
-    cudaFuncSetAttribute(level_sweep_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(level_sweep_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    cudaFuncSetAttribute(level_sweep_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     done = true;
   }
 }
 
 void launch_level_sweep(cudaStream_t s, const LevelArgs& a) {
-  if (a.has_old) level_sweep_kernel<true><<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
-  else level_sweep_kernel<false><<<1, LEVEL_NT, level_smem_bytes(a), s>>>(a);
+  const size_t smem = level_smem_bytes(a);
+  if (a.cluster <= 1) {
+    if (a.has_old) level_sweep_kernel<true, false><<<1, LEVEL_NT, smem, s>>>(a);
+    else level_sweep_kernel<false, false><<<1, LEVEL_NT, smem, s>>>(a);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.cluster, 1, 1);
+  cfg.blockDim = dim3(LEVEL_NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.cluster;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (a.has_old) cudaLaunchKernelEx(&cfg, level_sweep_kernel<true, true>, a);
+  else cudaLaunchKernelEx(&cfg, level_sweep_kernel<false, true>, a);
 }
 
 void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out) {

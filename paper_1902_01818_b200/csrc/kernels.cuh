@@ -54,6 +54,7 @@ struct LevelArgs {
   double* xp;         // solution in level order
   int TPR, R;
   int has_old;        // some entries read values outside the shared ring
+  int cluster;        // CTAs per sweep (thread-block cluster when > 1)
   long long* dbg;     // nullable: clock64 totals of thread 0 (debug)
   int ablate;         // debug: bit0 skip loads, bit1 skip dot, bit2 skip reduce+store
 };

@@ -144,3 +144,41 @@ def test_bad_arguments_are_errors():
     with pytest.raises(IgbError):
         ctx.finalize()                 # incomplete hierarchy
     ctx.close()
+
+
+@pytest.mark.slow
+def test_cfg4_p2_full_size_matches_reference_golden():
+    """cfg4 p=2 at full size (N = 1,054,729; 16 distorted patches; 7 levels).
+
+    Reference golden (tools/make_golden.py, igamg run here): 5 iterations, history, and a strided
+    sample of x.  The device GS here runs as a thread-block cluster (levels of ~256 rows).
+    """
+    g = load_golden("cfg4_p2")
+    pr, setup, f, solver, orc = device_solver("cfg4", p=2)
+    assert np.abs(f[:: int(g["x_sample_step"])] - g["f_sample"]).max() <= 1e-13 * np.abs(g["f_sample"]).max()
+    rep = solver.solve_pcg(f, check_spd=False)
+    assert rep.iterations == int(g["its"])
+    _check_history(rep.residuals, g["hist"], "cfg4 p=2 vs reference golden")
+    xs = rep.x[:: int(g["x_sample_step"])]
+    assert np.linalg.norm(xs - g["x_sample"]) <= 1e-10 * np.linalg.norm(g["x_sample"])
+
+
+def test_gs_cluster_path_matches_oracle():
+    """Force the clustered sweep on a small level (IGB_GS_CLUSTER) and compare with SuperLU."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup("cfg3", levels=2)
+    os.environ["IGB_GS_FORCE_CLUSTER"] = "3"
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_GS_FORCE_CLUSTER"]
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(9)
+    for level in (1, 2):
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        assert rel(solver.ctx.op("gs_fwd", level, x, n), orc.gs_forward(level, x)) <= 1e-12
+        assert rel(solver.ctx.op("gs_bwd", level, x, n), orc.gs_backward(level, x)) <= 1e-12
+    solver.close()

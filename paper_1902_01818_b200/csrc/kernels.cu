@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
   };
   constexpr int PF = 10;
   auto l2_prefetch = [&](int t) {
-    if (tid != LEVEL_NT - 1 || t >= T) return;
+    if (tid != LEVEL_NT - 1 || t >= T || (a.ablate & 8)) return;
     const int4 m = __ldg(meta + t);
     const long long off = 16LL * m.x;
     const long long end = (t + 1 < T) ? 16LL * __ldg(meta + t + 1).x : off + 16;

@@ -111,6 +111,80 @@ __global__ void lat(long long* out, double a, float af) {
   out[3] = (long long)(x + z + f);
 }
 
+// Early/late split: warps 0..LW-1 own rows (late part: 2 entries + partial from smem),
+// the other warps compute the early partial sums of the next step into smem.
+template <int TPR>
+__global__ void __launch_bounds__(NT) probe_split(const double2* vs, const int2* cs, const double* rp, double* xp,
+                                                  int T, int nrows, long long* out) {
+  __shared__ double ring[4096];
+  __shared__ double part[2][256];
+  const int tid = threadIdx.x;
+  for (int i = tid; i < 4096; i += NT) ring[i] = 0.0;
+  for (int i = tid; i < 512; i += NT) (&part[0][0])[i] = 0.0;
+  __syncthreads();
+  const int nthr = nrows * TPR;            // early-part threads (helpers), TPR per row
+  const bool helper = tid >= 128 && tid - 128 < nthr;
+  const int htid = tid - 128, hrho = htid / TPR, htau = htid % TPR;
+  const bool owner = tid < nrows;          // late part: one thread per row
+  const long long step_elems = (long long)nthr * (KMAX / 2);
+  Set A, B;
+  for (int k = 0; k < KMAX; ++k) { A.v[k] = B.v[k] = 0; A.c[k] = B.c[k] = k; }
+  A.b = B.b = 0; A.invd = B.invd = 0.5;
+  auto load = [&](Set& S, int t) {
+    if (!helper) return;
+    const double2* v2 = vs + (long long)t * step_elems + htid;
+    const int2* c2 = cs + (long long)t * step_elems + htid;
+#pragma unroll
+    for (int j = 0; j < KMAX / 2; ++j) {
+      const double2 a = __ldg(v2 + j * nthr);
+      const int2 b = __ldg(c2 + j * nthr);
+      S.v[2 * j] = a.x; S.v[2 * j + 1] = a.y; S.c[2 * j] = b.x; S.c[2 * j + 1] = b.y;
+    }
+  };
+  double lv0 = 0.1, lv1 = 0.2, b = 0.0;
+  long long t0 = clock64();
+  load(A, 0);
+  for (int t = 0; t < T; t += 2) {
+    // helpers: early part of step t+1 (uses ring values of steps <= t-1)
+    load(B, t + 1);
+    {
+      double s0 = 0, s1 = 0;
+      if (helper) {
+#pragma unroll
+        for (int k = 0; k < KMAX; k += 2) { s0 = fma(A.v[k], ring[A.c[k] & 4095], s0); s1 = fma(A.v[k + 1], ring[A.c[k + 1] & 4095], s1); }
+      }
+      double s = s0 + s1;
+      for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (helper && htau == 0) part[(t + 1) & 1][hrho] = s;
+    }
+    if (owner) {  // late part of step t: 2 entries from the previous step + partial
+      const double xi = (b - part[t & 1][tid] - lv0 * ring[(tid + 3) & 4095] - lv1 * ring[(tid + 5) & 4095]) * 0.5;
+      ring[(t * nrows + tid) & 4095] = xi;
+      xp[(long long)t * nrows + tid] = xi;
+    }
+    __syncthreads();
+    load(A, t + 2);
+    {
+      double s0 = 0, s1 = 0;
+      if (helper) {
+#pragma unroll
+        for (int k = 0; k < KMAX; k += 2) { s0 = fma(B.v[k], ring[B.c[k] & 4095], s0); s1 = fma(B.v[k + 1], ring[B.c[k + 1] & 4095], s1); }
+      }
+      double s = s0 + s1;
+      for (int o = TPR >> 1; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (helper && htau == 0) part[t & 1][hrho] = s;
+    }
+    if (owner) {
+      const double xi = (b - part[(t + 1) & 1][tid] - lv0 * ring[(tid + 3) & 4095] - lv1 * ring[(tid + 5) & 4095]) * 0.5;
+      ring[((t + 1) * nrows + tid) & 4095] = xi;
+      xp[(long long)(t + 1) * nrows + tid] = xi;
+    }
+    __syncthreads();
+  }
+  long long t1 = clock64();
+  if (tid == 0) out[0] = (t1 - t0) / T;
+}
+
 int main() {
   const int T = 1300, nrows = 52;
   const long long elems = (long long)(T + 8) * nrows * 8 * (KMAX / 2);
@@ -123,6 +197,13 @@ int main() {
     long long h[4];
     cudaMemcpy(h, out, 32, cudaMemcpyDeviceToHost);
     printf("dependent DFMA %lld cyc, DADD %lld cyc, FFMA %lld cyc (incl. loop overhead)\n", h[0], h[1], h[2]);
+  }
+  {
+    probe_split<4><<<1, NT>>>(vs, cs, rp, xp, T, nrows, out);
+    probe_split<4><<<1, NT>>>(vs, cs, rp, xp, T, nrows, out);
+    long long h;
+    cudaMemcpy(&h, out, 8, cudaMemcpyDeviceToHost);
+    printf("early/late split (helpers 6 warps, 1-set loads) rows 52: %lld cyc/step\n", h);
   }
   run<0, 4>(vs, cs, rp, xp, T, nrows, out, "barrier only");
   run<22, 4>(vs, cs, rp, xp, T, nrows, out, "tree-dot+shfl+store");

@@ -22,6 +22,7 @@
 
 #include "igb.h"
 #include "level_plan.h"
+#include "panel_plan.h"
 #include "kernels.cuh"
 
 using namespace igb;
@@ -91,12 +92,21 @@ struct SweepDev {
   double stream_bytes = 0;
 };
 
+struct PanelDev {
+  bool ok = false;
+  PanelArgs args{};
+  long long npan = 0, near = 0, far = 0;
+  double lin_bytes = 0, ent_bytes = 0;
+};
+
 struct Level {
   int n = 0;
   DevCsr A;
   std::vector<int> h_ptr, h_col;
   std::vector<double> h_val;
   SweepDev sweep[2];   // 0: forward (lower) sweep, 1: backward (upper) sweep
+  PanelDev panel[2];   // row-panel sweeps (preferred when built)
+  double* xg = nullptr;  // panel sweep solution by position (old values)
   double* rp = nullptr;   // level-ordered right-hand side / solution of the sweep
   double* xp = nullptr;
   std::vector<double> h_diag;
@@ -276,6 +286,35 @@ struct igb_ctx {
   // accumulated into u.
   void gs(int l, bool upper, const double* rhs, double* u, bool u_zero) {
     Level& V = lev[l];
+    PanelDev& Pn = V.panel[upper ? 1 : 0];
+    if (Pn.ok) {
+      PanelArgs a = Pn.args;
+      a.res = rhs;
+      a.u = u;
+      a.accumulate = u_zero ? 0 : 1;
+      static long long* dbg = nullptr;
+      static const bool want_dbg = std::getenv("IGB_GS_DEBUG") != nullptr;
+      if (want_dbg && !capturing) {
+        if (!dbg) CU(cudaMalloc(&dbg, 8 * sizeof(long long)));
+        a.dbg = dbg;
+        const char* ab = std::getenv("IGB_GS_ABLATE");
+        a.ablate = ab ? std::atoi(ab) : 0;
+      }
+      const double bytes = Pn.lin_bytes + Pn.ent_bytes + 8.0 * V.n * (u_zero ? 2 : 3);
+      launch(K_GS, bytes, [&] { launch_panel_sweep(stream, a); });
+      if (a.dbg) {
+        long long hd[8];
+        CU(cudaMemcpyAsync(hd, dbg, sizeof(hd), cudaMemcpyDeviceToHost, stream));
+        CU(cudaStreamSynchronize(stream));
+        const long long np = hd[0] > 0 ? hd[0] : 1;
+        std::fprintf(stderr,
+                     "[gs dbg] panel level %d dir %d n %d panels %lld: %lld cyc/panel (wait_x %lld, loads %lld, "
+                     "phaseA %lld, wait_r %lld, wait_tma %lld, phaseB %lld)\n",
+                     l, upper ? 1 : 0, V.n, hd[0], hd[1] / np, hd[2] / np, hd[3] / np, hd[4] / np, hd[5] / np,
+                     hd[6] / np, hd[7] / np);
+      }
+      return;
+    }
     SweepDev& C = V.sweep[upper ? 1 : 0];
     if (C.ok) {
       LevelArgs a = C.args;
@@ -823,6 +862,76 @@ int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long
   });
 }
 
+// Row-panel sweep for one direction (panel_plan.h).  Chosen when the panel chain
+// (npan) is clearly shorter than the DAG depth (nlev) or when forced; cluster of 16
+// CTAs (B = 512) if the device can host it, else 8 (B = 256).
+bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp, int nlev,
+                       bool force) {
+  static int G = -1;
+  if (G < 0) {
+    G = 0;
+    const char* genv = std::getenv("IGB_PANEL_G");
+    const int want = genv ? std::atoi(genv) : 16;
+    for (int g : {16, 8})
+      if (g <= want && panel_prepare(g, g + 1)) {
+        G = g;
+        break;
+      }
+  }
+  if (!G) return false;
+  const int B = 32 * G;
+  const int npan = (V.n + B - 1) / B;
+  if (!force && 2 * npan > nlev) return false;
+  PanelPlanHost plan;
+  const int R = 8192;
+  if (!build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, R, plan))
+    return false;
+  PanelDev& P = V.panel[dir];
+  PanelArgs& a = P.args;
+  a = PanelArgs{};
+  a.n = V.n;
+  a.npan = plan.npan;
+  a.B = plan.B;
+  a.R = plan.R;
+  a.G = plan.G;
+  a.KBC = plan.KBC;
+  a.KA = plan.KA;
+  a.KF = plan.KF;
+  a.upper = dir;
+  const char* st = std::getenv("IGB_PANEL_STAGES");
+  a.stages = st ? std::max(0, std::atoi(st)) : 2;  // 0: inverse entries in registers (LREG)
+  if (a.stages == 1) a.stages = 2;
+  const char* pf = std::getenv("IGB_PANEL_PF");
+  a.pf = pf ? std::max(0, std::atoi(pf)) : 2;
+  while (a.stages > 2 && panel_smem_bytes(a) > 227u * 1024) --a.stages;
+  if (panel_smem_bytes(a) > 227u * 1024) return false;
+  a.lin = ctx->upload(plan.lin.data(), plan.lin.size());
+  a.ev = ctx->upload(plan.ev.data(), plan.ev.size());
+  a.ec = ctx->upload(plan.ec.data(), plan.ec.size());
+  if (plan.KF > 0) {
+    a.fv = ctx->upload(plan.fv.data(), plan.fv.size());
+    a.fc = ctx->upload(plan.fc.data(), plan.fc.size());
+    if (!V.xg) {
+      V.xg = ctx->alloc<double>(V.n);
+      CU(cudaMemset(V.xg, 0, sizeof(double) * V.n));  // padded far entries read position 0
+    }
+    a.xg = V.xg;
+  }
+  P.npan = plan.npan;
+  P.near = plan.near_entries;
+  P.far = plan.far_entries;
+  P.lin_bytes = 8.0 * plan.lin.size();
+  P.ent_bytes = 12.0 * plan.ev.size() + 12.0 * plan.fv.size() * plan.npan / (plan.npan + 1);
+  P.ok = true;
+  if (std::getenv("IGB_VERBOSE"))
+    std::fprintf(stderr,
+                 "[igb] level %d dir %d: panel sweep n %d depth %d panels %d (G %d B %d) KA %d KF %d near %lld far %lld "
+                 "inverse %.1f MB growth %.2f smem %zu stages %d\n",
+                 level, dir, V.n, nlev, plan.npan, plan.G, plan.B, plan.KA, plan.KF, plan.near_entries,
+                 plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a), a.stages);
+  return true;
+}
+
 int igb_set_gs(igb_ctx* ctx, int level) {
   return guarded(ctx, [&] {
     require_levels(ctx);
@@ -832,11 +941,20 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);
     V.bwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, true);
     const char* eng = std::getenv("IGB_GS_ENGINE");
-    const bool want_stream = !(eng && std::string(eng) == "levels");
+    const std::string engine = eng ? eng : "auto";
+    const bool want_stream = engine != "levels";
+    bool panel_done[2] = {false, false};
+    if (engine == "auto" || engine == "panel") {
+      for (int dir = 0; dir < 2; ++dir) {
+        const Sched& Sd = dir ? V.bwd : V.fwd;
+        panel_done[dir] = build_panel_sweep(ctx, V, level, dir, dp, Sd.nlev, engine == "panel");
+      }
+    }
     level_prepare();
     const char* clenv = std::getenv("IGB_GS_CLUSTER");
     const int cluster_max = clenv ? std::max(1, std::min(8, std::atoi(clenv))) : 8;
     for (int dir = 0; dir < 2 && want_stream; ++dir) {
+      if (panel_done[dir]) continue;
       SweepDev& C = V.sweep[dir];
       LevelPlanHost plan;
       LevelArgs& a = C.args;

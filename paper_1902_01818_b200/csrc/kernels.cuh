@@ -67,6 +67,30 @@ void launch_level_sweep(cudaStream_t s, const LevelArgs& a);
 void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out);
 void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* xp, double* u, int accumulate);
 
+// ---- row-panel triangular sweep (Gauss-Seidel in natural order), one cluster ----
+// See panel_plan.h: G CTAs x PANEL_W warps, panels of B = 32 G rows, inverse blocks
+// streamed by TMA, recent solution values in a DSMEM-broadcast ring of R slots.
+constexpr int PANEL_W = 16;
+struct PanelArgs {
+  const double* lin;  // [npan][G][W][KBC][32]
+  const double* ev;   // [npan][G][W][KA][32]
+  const int* ec;
+  const double* fv;   // [npan][G][W][KF][32]
+  const int* fc;
+  const double* res;  // right-hand side by row
+  double* u;          // u (+)= c by row
+  double* xg;         // c by position (only when KF > 0)
+  int n, npan, B, R, G, KBC, KA, KF;
+  int upper, accumulate, stages, pf;
+  long long* dbg;     // nullable: clock64 totals of CTA 0 thread 0 (debug)
+  int ablate;         // debug: bit0 no TMA, bit1 no cluster barriers, bit2 no inverse product,
+                      // bit3 local stores only, bit4 no phase-A gathers,
+                      // bit5 no u / xg traffic
+};
+size_t panel_smem_bytes(const PanelArgs& a);
+bool panel_prepare(int G, int KBC);   // false: no cluster of G CTAs fits this device
+void launch_panel_sweep(cudaStream_t s, const PanelArgs& a);
+
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
 // y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
 // out[i] = w[perm_c[i]].  Column j updates run in parallel; one barrier per column.

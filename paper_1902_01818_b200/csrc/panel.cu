@@ -1,0 +1,404 @@
+// panel.cu -- row-panel triangular sweep for the Gauss-Seidel smoother (sm_100a).
+//
+// Solves T c = r (T = tril(A) forward / triu(A) backward, smoothers.py:178-190) in
+// position space, one panel of B = 32 G rows per step, on one thread-block cluster
+// of G CTAs x 16 warps (plan: panel_plan.h).  Per panel k:
+//
+//   phase A  r_i = res_i - sum_{q < kB} T_iq c_q       half-warp per row, ring in smem
+//            (+ entries older than the ring, gathered one panel ahead from global)
+//            -> r_i stored into every CTA's rbuf (DSMEM);   cluster barrier
+//   phase B  c_i = sum_j Tinv_kk[i][j] r_j              warp per row pair (q, b-1-q),
+//            Tinv slice of this CTA staged by a TMA bulk copy issued `stages-1`
+//            panels ahead -> c_i stored into every CTA's ring (DSMEM), u, xg;
+//            cluster barrier
+//
+// Everything but c is x-independent and streamed ahead: the per-panel critical
+// path is two cluster barriers plus a 16-lane and a 32-lane reduction.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace igb {
+
+namespace {
+
+__device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init1(unsigned long long* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+      "l"(src), "r"(bytes), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "PWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra PWAIT_%=;\n}" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned mapa(unsigned local, int rank) {
+  unsigned r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local), "r"(rank));
+  return r;
+}
+// store one double into (remote) shared memory; completion is signalled on the
+// receiver's mbarrier as 8 transaction bytes
+__device__ __forceinline__ void st_async(unsigned raddr, double v, unsigned rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];" ::"r"(raddr),
+               "l"(__double_as_longlong(v)), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arm(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "CWAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra CWAIT_%=;\n}" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int KA, int KF, int KL>
+struct PanelSet {
+  double lv[KL];               // inverse entries (register variant)
+  double b, u0;
+  double ev[KA];
+  int ec[KA];
+  double fv[KF > 0 ? KF : 1];  // far coefficients of the NEXT panel
+  int fc[KF > 0 ? KF : 1];
+  double fx[KF > 0 ? KF : 1];  // their solution values (loaded one panel ahead)
+};
+
+// Synchronisation: no CTA-wide or cluster-wide barrier per panel.  Every value
+// a CTA needs from its peers arrives by st.async with a complete_tx on one of two
+// local mbarriers -- bar_r (the b_t residuals r of panel t) and bar_x (the b_t
+// solution values of panel t) -- which thread 0 re-arms with the byte count of the
+// next panel as soon as a phase completes.  A producer cannot run a phase ahead:
+// r(t+1) needs every CTA's x(t), and x(t) needs every r(t), so one mbarrier per
+// kind and a double-buffered rbuf suffice.  Old values read from global memory
+// (KF > 0) are ordered by a cluster barrier every R/B panels (a far value read
+// during panel t was written during a panel <= t - R/B).
+// LREG: the inverse slice of every warp is loaded straight into registers one panel
+// ahead (bulk L2 prefetch `pf` panels ahead) instead of TMA-staged in shared memory.
+
+template <int KBC, int KA, int KF, bool LREG>
+__global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs a) {
+  constexpr int KL = LREG ? KBC : 1;
+  using Set = PanelSet<KA, KF, KL>;
+  extern __shared__ __align__(128) double psm[];
+  constexpr int W = PANEL_W;
+  const int B = a.B, R = a.R, T = a.npan, n = a.n, S = a.stages;
+  const cg::cluster_group cluster = cg::this_cluster();
+  const int G = (int)cluster.num_blocks(), s = (int)cluster.block_rank();
+  const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, h = l >> 4, hl = l & 15;
+  const int pq = w * G + s;  // pair index: rows pq and b-1-pq of every panel
+  double* ring = psm;
+  double* rbuf = ring + R;                    // [2][B]
+  double* lin_s = rbuf + 2 * B;               // [S][W][KBC][32]
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(lin_s + (size_t)S * W * KBC * 32);
+  unsigned long long* full = bars;            // [S] TMA stages
+  unsigned long long* bar_r = bars + S;
+  unsigned long long* bar_x = bars + S + 1;
+  const size_t cta_lin = (size_t)W * KBC * 32;
+  const unsigned lin_bytes = (unsigned)(cta_lin * 8);
+  auto panel_rows = [&](int t) { return min(B, n - t * B); };
+
+  for (int i = tid; i < R + 2 * B; i += W * 32) psm[i] = 0.0;
+  if (tid == 0) {
+    for (int i = 0; i < S + 2; ++i) mbar_init1(&bars[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_arm(bar_r, 8u * panel_rows(0));
+    mbar_arm(bar_x, 8u * panel_rows(0));
+  }
+  // lane hl sends to CTA hl of the cluster (G <= 16)
+  const int peer = hl < G ? hl : 0;
+  const unsigned peer_psm = mapa(saddr(psm), peer);
+  const unsigned peer_bar_r = mapa(saddr(bar_r), peer), peer_bar_x = mapa(saddr(bar_x), peer);
+  cluster.sync();
+
+  const double* lin_g = a.lin + (size_t)s * cta_lin;
+  const size_t lin_panel = (size_t)G * cta_lin;
+  if (!LREG && tid == 0 && !(a.ablate & 1)) {
+    for (int t = 0; t < S - 1 && t < T; ++t)
+      bulk_load(lin_s + (size_t)t * cta_lin, lin_g + t * lin_panel, lin_bytes, &full[t]);
+    for (int t = S - 1; t < S - 1 + a.pf && t < T; ++t) bulk_prefetch_l2(lin_g + t * lin_panel, lin_bytes);
+  }
+
+  const size_t ent_cta = (size_t)W * KA * 32, far_cta = (size_t)W * KF * 32;
+  const size_t ent_off = ((size_t)s * W + w) * KA * 32 + l, far_off = ((size_t)s * W + w) * KF * 32 + l;
+  const int rmask = R - 1;
+  const int far_period = R / B;
+  const double* lin_w = lin_g + (size_t)w * KBC * 32 + l;  // this lane's inverse entries (LREG)
+  if (LREG && l == 0 && !(a.ablate & 1))
+    for (int t = 0; t < a.pf && t < T; ++t) bulk_prefetch_l2(lin_w + t * lin_panel, 8u * KBC * 32);
+
+  // set of panel t: rhs + old u + near entries of t, far entries of t+1
+  auto load = [&](Set& X, int t) {
+    const int k0 = t * B, b = panel_rows(t);
+    if (LREG) {
+      const double* lp = lin_w + t * lin_panel;
+#pragma unroll
+      for (int c = 0; c < KL; ++c) X.lv[c] = __ldg(lp + c * 32);
+      if (l == 0 && !(a.ablate & 1) && t + a.pf < T) bulk_prefetch_l2(lp + a.pf * lin_panel, 8u * KBC * 32);
+    }
+    const int pr = h ? b - 1 - pq : pq;
+    const int p = min(k0 + max(pr, 0), n - 1);  // clamped: invalid rows load a finite dummy
+    const int row = a.upper ? n - 1 - p : p;
+    X.b = __ldg(a.res + row);
+    X.u0 = a.u[row];
+    const size_t eo = (size_t)t * G * ent_cta + ent_off;
+#pragma unroll
+    for (int j = 0; j < KA; ++j) {
+      X.ev[j] = __ldg(a.ev + eo + j * 32);
+      X.ec[j] = __ldg(a.ec + eo + j * 32);
+    }
+    if (KF > 0) {
+      const size_t fo = (size_t)(t + 1) * G * far_cta + far_off;  // panel npan is a zero pad
+#pragma unroll
+      for (int j = 0; j < KF; ++j) {
+        X.fv[j] = __ldg(a.fv + fo + j * 32);
+        X.fc[j] = __ldg(a.fc + fo + j * 32);
+      }
+    }
+  };
+
+  Set A, Bs;
+  load(A, 0);
+#pragma unroll
+  for (int j = 0; j < (KF > 0 ? KF : 1); ++j) {
+    Bs.fv[j] = 0.0;
+    Bs.fx[j] = 0.0;
+  }
+  const long long t_start = clock64();
+  long long tm[6] = {0, 0, 0, 0, 0, 0};
+  long long tprev = t_start;
+  auto mark = [&](int i) {
+    if (a.dbg) {
+      const long long now = clock64();
+      tm[i] += now - tprev;
+      tprev = now;
+    }
+  };
+
+  auto step = [&](Set& X, Set& Y, int t) {
+    const int k0 = t * B, b = panel_rows(t);
+    if (t > 0) {  // x of panel t-1 complete in this CTA's ring
+      mbar_wait_cluster(bar_x, (unsigned)((t - 1) & 1));
+      if (tid == 0) mbar_arm(bar_x, 8u * b);
+    }
+    mark(0);
+    if (KF > 0 && t > 0 && t % far_period == 0) {
+      cluster_arrive();
+      cluster_wait();
+    }
+    // far part of panel t (values gathered during panel t-1)
+    double sA = 0.0;
+    if (KF > 0) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) sA = fma(Y.fv[j], Y.fx[j], sA);
+#pragma unroll
+      for (int j = 0; j < KF; ++j) X.fx[j] = __ldcg(a.xg + X.fc[j]);  // panel t+1: positions < tB - R + B
+    }
+    if (t + 1 < T) load(Y, t + 1);
+    if (!LREG && tid == 0 && !(a.ablate & 1)) {
+      const int tn = t + S - 1;  // refills the stage panel t-1 used (every warp is past it: bar_x)
+      if (tn < T) bulk_load(lin_s + (size_t)(tn % S) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn % S]);
+      if (a.pf && tn + a.pf < T) bulk_prefetch_l2(lin_g + (tn + a.pf) * lin_panel, lin_bytes);
+    }
+    mark(1);
+    // ---- phase A: off-panel part, half-warp per row
+    const int r1 = pq, r2 = b - 1 - pq;
+    const bool v1 = pq < (b + 1) / 2, v2 = pq < b / 2;
+    const bool vh = h ? v2 : v1;
+    const int pr = h ? r2 : r1;
+    if (!(a.ablate & 16)) {
+#pragma unroll
+      for (int j = 0; j < KA; ++j) sA = fma(X.ev[j], ring[X.ec[j]], sA);
+    }
+    sA += __shfl_xor_sync(0xffffffffu, sA, 8);
+    sA += __shfl_xor_sync(0xffffffffu, sA, 4);
+    sA += __shfl_xor_sync(0xffffffffu, sA, 2);
+    sA += __shfl_xor_sync(0xffffffffu, sA, 1);
+    const int rb = (t & 1) * B;
+    if (vh && hl < G) st_async(peer_psm + 8u * (R + rb + pr), X.b - sA, peer_bar_r);
+    mark(2);
+    // ---- phase B: inverse block, warp per row pair
+    mbar_wait_cluster(bar_r, (unsigned)(t & 1));
+    if (tid == 0 && t + 1 < T) mbar_arm(bar_r, 8u * panel_rows(t + 1));
+    mark(3);
+    if (!LREG && !(a.ablate & 1)) mbar_wait_parity(&full[t % S], (unsigned)((t / S) & 1));
+    mark(4);
+    const double* L = lin_s + (size_t)(LREG ? 0 : t % S) * cta_lin + (size_t)w * KBC * 32 + l;
+    const double* rv = rbuf + rb;
+    const int len1 = v1 ? r1 + 1 : 0;
+    double a1 = 0.0, a2 = 0.0;
+    if (a.ablate & 4) {
+      a1 = rv[l];
+      a2 = rv[l + 32];
+    } else {
+#pragma unroll
+      for (int c = 0; c < KBC; ++c) {
+        const int e = c * 32 + l;
+        const bool first = e < len1;
+        const int j = min(first ? e : e - len1, B - 1);
+        const double v = LREG ? X.lv[LREG ? c : 0] : L[c * 32];
+        const double x = rv[j];
+        a1 = fma(first ? v : 0.0, x, a1);
+        a2 = fma(first ? 0.0 : v, x, a2);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a1 += __shfl_xor_sync(0xffffffffu, a1, o);
+      a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+    }
+    const double xv = h ? a2 : a1;
+    if (vh) {
+      if (hl < G) st_async(peer_psm + 8u * ((k0 + pr) & rmask), xv, peer_bar_x);
+      if (hl == 0 && !(a.ablate & 32)) {
+        const int p = k0 + pr;
+        const int row = a.upper ? n - 1 - p : p;
+        a.u[row] = a.accumulate ? X.u0 + xv : xv;
+        if (KF > 0) __stcg(a.xg + p, xv);
+      }
+    }
+    mark(5);
+  };
+  for (int t = 0; t < T; t += 2) {
+    step(A, Bs, t);
+    if (t + 1 < T) step(Bs, A, t + 1);
+  }
+  // every x of the last panel has landed here before anyone leaves the cluster
+  mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1));
+  cluster.sync();
+  if (a.dbg && s == 0 && tid == 0) {
+    a.dbg[0] = T;
+    a.dbg[1] = clock64() - t_start;
+    for (int i = 0; i < 6; ++i) a.dbg[2 + i] = tm[i];
+  }
+}
+
+template <int KBC, int KA, int KF>
+void launch_one(cudaStream_t st, const PanelArgs& a) {
+  auto kern = a.stages == 0 ? panel_sweep_kernel<KBC, KA, KF, true> : panel_sweep_kernel<KBC, KA, KF, false>;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(a.G, 1, 1);
+  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.dynamicSmemBytes = panel_smem_bytes(a);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = a.G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, a);
+}
+
+template <int KBC, int KA>
+void dispatch_kf(cudaStream_t st, const PanelArgs& a) {
+  switch (a.KF) {
+    case 0: launch_one<KBC, KA, 0>(st, a); break;
+    case 1: launch_one<KBC, KA, 1>(st, a); break;
+    default: launch_one<KBC, KA, 4>(st, a); break;
+  }
+}
+
+template <int KBC>
+void dispatch_ka(cudaStream_t st, const PanelArgs& a) {
+  switch (a.KA) {
+    case 2: dispatch_kf<KBC, 2>(st, a); break;
+    case 4: dispatch_kf<KBC, 4>(st, a); break;
+    case 8: dispatch_kf<KBC, 8>(st, a); break;
+    default: dispatch_kf<KBC, 12>(st, a); break;
+  }
+}
+
+template <class F>
+void for_all_variants(int KBC, F&& f) {
+  auto per_ka = [&](auto kbc, auto ka) {
+    constexpr int C = decltype(kbc)::value, K = decltype(ka)::value;
+    f(panel_sweep_kernel<C, K, 0, false>);
+    f(panel_sweep_kernel<C, K, 1, false>);
+    f(panel_sweep_kernel<C, K, 4, false>);
+    f(panel_sweep_kernel<C, K, 0, true>);
+    f(panel_sweep_kernel<C, K, 1, true>);
+    f(panel_sweep_kernel<C, K, 4, true>);
+  };
+  auto per_kbc = [&](auto kbc) {
+    per_ka(kbc, std::integral_constant<int, 2>{});
+    per_ka(kbc, std::integral_constant<int, 4>{});
+    per_ka(kbc, std::integral_constant<int, 8>{});
+    per_ka(kbc, std::integral_constant<int, 12>{});
+  };
+  if (KBC == 17) per_kbc(std::integral_constant<int, 17>{});
+  else per_kbc(std::integral_constant<int, 9>{});
+}
+
+}  // namespace
+
+size_t panel_smem_bytes(const PanelArgs& a) {
+  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)a.stages * PANEL_W * a.KBC * 32) + 8 * ((size_t)a.stages + 2);
+}
+
+bool panel_prepare(int G, int KBC) {
+  if (KBC != 17 && KBC != 9) return false;
+  bool ok = true;
+  for_all_variants(KBC, [&](auto kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
+      ok = false;
+    if (G > 8 && cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      ok = false;
+  });
+  if (!ok) {
+    cudaGetLastError();
+    return false;
+  }
+  // can a cluster of G CTAs with (nearly) all shared memory be resident?
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G, 1, 1);
+  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.dynamicSmemBytes = 220 * 1024;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 0, false>, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 0, false>, &cfg);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return nclusters >= 1;
+}
+
+void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {
+  if (a.KBC == 17) dispatch_ka<17>(st, a);
+  else dispatch_ka<9>(st, a);
+}
+
+}  // namespace igb

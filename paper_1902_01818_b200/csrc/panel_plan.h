@@ -1,0 +1,51 @@
+// panel_plan.h -- host planner for the row-panel triangular sweep (one thread-block cluster).
+//
+// A Gauss-Seidel sweep in the reference's natural order (smoothers.py:178-190) is
+// the triangular solve T c = r with T = tril(A) (forward) or triu(A) (backward).
+// In *position* space (p = i forward, p = n-1-i backward) T is lower triangular.
+// The positions are cut into panels of B consecutive rows; for panel k
+//
+//     c_k = T_kk^{-1} (r_k - T_{k,<k} c_{<k})
+//
+// which is the same solve reassociated: the dependency chain is n/B panels long
+// instead of the DAG depth (1303 levels on the cfg2 finest level, 171 panels of
+// 393 rows or 132 of 512).  T_kk^{-1} is dense lower triangular and computed here
+// once per setup (fp64 row recurrence; |T_kk^{-1}| |T_kk| stays O(1) for these
+// matrices, tests/test_gpu_parity.py holds the sweep to 1e-12 of SuperLU).
+//
+// Device work split (G CTAs of W = B/(2G) warps): panel rows are paired
+// (q, b-1-q) so every pair owns b+1 inverse entries; pair q belongs to CTA q % G,
+// warp q / G.  Per panel and CTA the planner emits
+//   lin [W][KBC][32]    inverse rows of the warp's pair, concatenated (row q then
+//                       row b-1-q), entry e at chunk e/32, lane e%32, zero padded;
+//   ev/ec [W][KA][32]   off-panel coefficients with ring slots (position & (R-1)),
+//                       lanes 0-15 row q, lanes 16-31 row b-1-q, entry j at
+//                       slot j/16, lane j%16;
+//   fv/fc [W][KF][32]   off-panel coefficients older than the ring (position < kB-R),
+//                       read from the global position-ordered solution.
+#pragma once
+#include <vector>
+
+namespace igb {
+
+struct PanelPlanHost {
+  int n = 0;
+  int B = 512, G = 16, W = 16, R = 8192;
+  int KBC = 17, KA = 0, KF = 0;
+  int npan = 0;
+  long long near_entries = 0, far_entries = 0;
+  double max_inv_ratio = 0;  // max_k |T_kk^-1|_max * |T_kk|_max (growth diagnostic)
+  std::vector<double> lin;   // [npan][G][W][KBC][32]
+  std::vector<double> ev;    // [npan][G][W][KA][32]
+  std::vector<int> ec;
+  std::vector<double> fv;    // [npan + 1][G][W][KF][32] (last panel: zero pad)
+  std::vector<int> fc;
+};
+
+// Dependencies of row r: entries [ptr[r], dpos[r]) (lower) or (dpos[r], ptr[r+1])
+// (upper), diagonal val[dpos[r]].  Returns false when a row has more off-panel
+// entries than the kernel variants cover (KA > 12 or KF > 4).
+bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos,
+                      bool upper, int G, int R, PanelPlanHost& out);
+
+}  // namespace igb

@@ -908,6 +908,8 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   a.lin = ctx->upload(plan.lin.data(), plan.lin.size());
   a.ev = ctx->upload(plan.ev.data(), plan.ev.size());
   a.ec = ctx->upload(plan.ec.data(), plan.ec.size());
+  a.xmask = ctx->upload(plan.xmask.data(), plan.xmask.size());
+  a.xcnt = ctx->upload(plan.xcnt.data(), plan.xcnt.size());
   if (plan.KF > 0) {
     a.fv = ctx->upload(plan.fv.data(), plan.fv.size());
     a.fc = ctx->upload(plan.fc.data(), plan.fc.size());
@@ -926,9 +928,10 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   if (std::getenv("IGB_VERBOSE"))
     std::fprintf(stderr,
                  "[igb] level %d dir %d: panel sweep n %d depth %d panels %d (G %d B %d) KA %d KF %d near %lld far %lld "
-                 "inverse %.1f MB growth %.2f smem %zu stages %d\n",
+                 "inverse %.1f MB growth %.2f smem %zu stages %d x-messages/value %.2f\n",
                  level, dir, V.n, nlev, plan.npan, plan.G, plan.B, plan.KA, plan.KF, plan.near_entries,
-                 plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a), a.stages);
+                 plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a), a.stages,
+                 double(plan.x_messages) / V.n);
   return true;
 }
 

@@ -77,6 +77,8 @@ struct PanelArgs {
   const int* ec;
   const double* fv;   // [npan][G][W][KF][32]
   const int* fc;
+  const unsigned short* xmask;  // [npan*B] destination CTAs of each solution value
+  const int* xcnt;              // [npan+1][G] values each CTA receives per panel
   const double* res;  // right-hand side by row
   double* u;          // u (+)= c by row
   double* xg;         // c by position (only when KF > 0)

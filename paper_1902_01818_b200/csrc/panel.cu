@@ -17,6 +17,8 @@
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include "kernels.cuh"
 
 namespace cg = cooperative_groups;
@@ -67,20 +69,36 @@ __device__ __forceinline__ void st_async(unsigned raddr, double v, unsigned rbar
 __device__ __forceinline__ void mbar_arm(unsigned long long* b, unsigned bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity) {
+__device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity) {
+  unsigned ok;
   asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "CWAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra CWAIT_%=;\n}" ::"r"(saddr(b)),
-      "r"(parity)
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n}"
+      : "=r"(ok)
+      : "r"(saddr(b)), "r"(parity)
       : "memory");
+  return ok != 0;
+}
+// Wait for a phase of an exchange mbarrier.  Watchdog: a protocol error must not hang
+// the device -- after ~2^31 cycles report and trap (the launch fails with an error).
+__device__ __noinline__ void exchange_stuck(int what, int t, unsigned parity) {
+  printf("[igb panel] CTA %d thread %d: %s exchange of panel %d (parity %u) never completed\n",
+         (int)cg::this_cluster().block_rank(), (int)threadIdx.x, what ? "solution" : "residual", t, parity);
+  __trap();
+}
+__device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity, int what = 0, int t = 0) {
+  if (mbar_try(b, parity)) return;
+  const long long t0 = clock64();
+  while (!mbar_try(b, parity))
+    if (clock64() - t0 > (1LL << 31)) exchange_stuck(what, t, parity);
 }
 
 template <int KA, int KF, int KL>
 struct PanelSet {
   double lv[KL];               // inverse entries (register variant)
   double b, u0;
+  int xm, xc;                  // destination mask of this lane's phase-B row; values due in bar_x
   double ev[KA];
   int ec[KA];
   double fv[KF > 0 ? KF : 1];  // far coefficients of the NEXT panel
@@ -89,12 +107,18 @@ struct PanelSet {
 };
 
 // Synchronisation: no CTA-wide or cluster-wide barrier per panel.  Every value
-// a CTA needs from its peers arrives by st.async with a complete_tx on one of two
-// local mbarriers -- bar_r (the b_t residuals r of panel t) and bar_x (the b_t
-// solution values of panel t) -- which thread 0 re-arms with the byte count of the
-// next panel as soon as a phase completes.  A producer cannot run a phase ahead:
-// r(t+1) needs every CTA's x(t), and x(t) needs every r(t), so one mbarrier per
-// kind and a double-buffered rbuf suffice.  Old values read from global memory
+// a CTA needs from its peers arrives by st.async with a complete_tx on a local
+// mbarrier: bar_r[t & 1] counts the b_t residuals of panel t (broadcast to every
+// CTA), bar_x the solution values of panel t this CTA reads later (xcnt[t][cta];
+// each value goes only to the CTAs whose rows reference it).  Thread 0 re-arms a
+// barrier right after its phase completes, before its warp produces anything the
+// next phase depends on.  Ordering argument: a CTA sends r(t+2) only after the
+// x(t+1) it needs, which were produced after every CTA sent r(t+1), i.e. after
+// every warp finished panel t (wait_r(t), phase B(t)) -- the planner gives every
+// CTA at least one value of every panel so this holds; hence bar_r needs two
+// parities, rbuf two buffers, and after wait_r(t) every local warp is past phase
+// B(t-1) (so the TMA stage of panel t-1 may be refilled).  x(t+1) is produced only
+// after every CTA sent r(t+1), i.e. after its wait_x(t): one bar_x suffices.  Old values read from global memory
 // (KF > 0) are ordered by a cluster barrier every R/B panels (a far value read
 // during panel t was written during a panel <= t - R/B).
 // LREG: the inverse slice of every warp is loaded straight into registers one panel
@@ -116,23 +140,24 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   double* lin_s = rbuf + 2 * B;               // [S][W][KBC][32]
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(lin_s + (size_t)S * W * KBC * 32);
   unsigned long long* full = bars;            // [S] TMA stages
-  unsigned long long* bar_r = bars + S;
-  unsigned long long* bar_x = bars + S + 1;
+  unsigned long long* bar_r = bars + S;      // [2]
+  unsigned long long* bar_x = bars + S + 2;
   const size_t cta_lin = (size_t)W * KBC * 32;
   const unsigned lin_bytes = (unsigned)(cta_lin * 8);
   auto panel_rows = [&](int t) { return min(B, n - t * B); };
 
   for (int i = tid; i < R + 2 * B; i += W * 32) psm[i] = 0.0;
   if (tid == 0) {
-    for (int i = 0; i < S + 2; ++i) mbar_init1(&bars[i]);
+    for (int i = 0; i < S + 3; ++i) mbar_init1(&bars[i]);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_arm(bar_r, 8u * panel_rows(0));
-    mbar_arm(bar_x, 8u * panel_rows(0));
+    mbar_arm(&bar_r[0], 8u * panel_rows(0));
+    if (T > 1) mbar_arm(&bar_r[1], 8u * panel_rows(1));
+    mbar_arm(bar_x, 8u * __ldg(a.xcnt + s));
   }
   // lane hl sends to CTA hl of the cluster (G <= 16)
   const int peer = hl < G ? hl : 0;
   const unsigned peer_psm = mapa(saddr(psm), peer);
-  const unsigned peer_bar_r = mapa(saddr(bar_r), peer), peer_bar_x = mapa(saddr(bar_x), peer);
+  const unsigned peer_bar_r = mapa(saddr(bar_r), peer), peer_bar_x = mapa(saddr(bar_x), peer);  // + 8 (t & 1)
   cluster.sync();
 
   const double* lin_g = a.lin + (size_t)s * cta_lin;
@@ -154,6 +179,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   // set of panel t: rhs + old u + near entries of t, far entries of t+1
   auto load = [&](Set& X, int t) {
     const int k0 = t * B, b = panel_rows(t);
+    const int ia = s * (B / G) + 2 * w + h;  // phase-A row (contiguous chunk per CTA)
     if (LREG) {
       const double* lp = lin_w + t * lin_panel;
 #pragma unroll
@@ -163,8 +189,11 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     const int pr = h ? b - 1 - pq : pq;
     const int p = min(k0 + max(pr, 0), n - 1);  // clamped: invalid rows load a finite dummy
     const int row = a.upper ? n - 1 - p : p;
-    X.b = __ldg(a.res + row);
-    X.u0 = a.u[row];
+    const int pa = min(k0 + ia, n - 1);
+    X.b = __ldg(a.res + (a.upper ? n - 1 - pa : pa));
+    if (a.accumulate) X.u0 = a.u[row];
+    X.xm = __ldg(a.xmask + p);
+    X.xc = __ldg(a.xcnt + (size_t)t * G + s);
     const size_t eo = (size_t)t * G * ent_cta + ent_off;
 #pragma unroll
     for (int j = 0; j < KA; ++j) {
@@ -202,8 +231,8 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   auto step = [&](Set& X, Set& Y, int t) {
     const int k0 = t * B, b = panel_rows(t);
     if (t > 0) {  // x of panel t-1 complete in this CTA's ring
-      mbar_wait_cluster(bar_x, (unsigned)((t - 1) & 1));
-      if (tid == 0) mbar_arm(bar_x, 8u * b);
+      mbar_wait_cluster(bar_x, (unsigned)((t - 1) & 1), 1, t - 1);
+      if (tid == 0) mbar_arm(bar_x, 8u * X.xc);
     }
     mark(0);
     if (KF > 0 && t > 0 && t % far_period == 0) {
@@ -215,14 +244,6 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     if (KF > 0) {
 #pragma unroll
       for (int j = 0; j < KF; ++j) sA = fma(Y.fv[j], Y.fx[j], sA);
-#pragma unroll
-      for (int j = 0; j < KF; ++j) X.fx[j] = __ldcg(a.xg + X.fc[j]);  // panel t+1: positions < tB - R + B
-    }
-    if (t + 1 < T) load(Y, t + 1);
-    if (!LREG && tid == 0 && !(a.ablate & 1)) {
-      const int tn = t + S - 1;  // refills the stage panel t-1 used (every warp is past it: bar_x)
-      if (tn < T) bulk_load(lin_s + (size_t)(tn % S) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn % S]);
-      if (a.pf && tn + a.pf < T) bulk_prefetch_l2(lin_g + (tn + a.pf) * lin_panel, lin_bytes);
     }
     mark(1);
     // ---- phase A: off-panel part, half-warp per row
@@ -239,11 +260,25 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     sA += __shfl_xor_sync(0xffffffffu, sA, 2);
     sA += __shfl_xor_sync(0xffffffffu, sA, 1);
     const int rb = (t & 1) * B;
-    if (vh && hl < G) st_async(peer_psm + 8u * (R + rb + pr), X.b - sA, peer_bar_r);
+    const int ia = s * (B / G) + 2 * w + h;
+    if (ia < b && hl < G) st_async(peer_psm + 8u * (R + rb + ia), X.b - sA, peer_bar_r + 8u * (t & 1));
+    // issued while the residual exchange is in flight: next panel's set, old values
+    if (KF > 0) {
+#pragma unroll
+      for (int j = 0; j < KF; ++j) X.fx[j] = __ldcg(a.xg + X.fc[j]);  // panel t+1: positions < tB - R + B
+    }
+    if (t + 1 < T) load(Y, t + 1);
     mark(2);
     // ---- phase B: inverse block, warp per row pair
-    mbar_wait_cluster(bar_r, (unsigned)(t & 1));
-    if (tid == 0 && t + 1 < T) mbar_arm(bar_r, 8u * panel_rows(t + 1));
+    mbar_wait_cluster(&bar_r[t & 1], (unsigned)((t >> 1) & 1), 0, t);
+    if (tid == 0) {
+      if (t + 2 < T) mbar_arm(&bar_r[t & 1], 8u * panel_rows(t + 2));
+      const int tn = t + S - 1;  // stage of panel t-1: every local warp is past it (wait_r)
+      if (!LREG && !(a.ablate & 1)) {
+        if (tn < T) bulk_load(lin_s + (size_t)(tn % S) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn % S]);
+        if (a.pf && tn + a.pf < T) bulk_prefetch_l2(lin_g + (tn + a.pf) * lin_panel, lin_bytes);
+      }
+    }
     mark(3);
     if (!LREG && !(a.ablate & 1)) mbar_wait_parity(&full[t % S], (unsigned)((t / S) & 1));
     mark(4);
@@ -273,7 +308,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     }
     const double xv = h ? a2 : a1;
     if (vh) {
-      if (hl < G) st_async(peer_psm + 8u * ((k0 + pr) & rmask), xv, peer_bar_x);
+      if (hl < G && (X.xm >> hl & 1)) st_async(peer_psm + 8u * ((k0 + pr) & rmask), xv, peer_bar_x);
       if (hl == 0 && !(a.ablate & 32)) {
         const int p = k0 + pr;
         const int row = a.upper ? n - 1 - p : p;
@@ -288,7 +323,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     if (t + 1 < T) step(Bs, A, t + 1);
   }
   // every x of the last panel has landed here before anyone leaves the cluster
-  mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1));
+  mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1), 1, T - 1);
   cluster.sync();
   if (a.dbg && s == 0 && tid == 0) {
     a.dbg[0] = T;
@@ -358,7 +393,7 @@ void for_all_variants(int KBC, F&& f) {
 }  // namespace
 
 size_t panel_smem_bytes(const PanelArgs& a) {
-  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)a.stages * PANEL_W * a.KBC * 32) + 8 * ((size_t)a.stages + 2);
+  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)a.stages * PANEL_W * a.KBC * 32) + 8 * ((size_t)a.stages + 3);
 }
 
 bool panel_prepare(int G, int KBC) {

@@ -112,9 +112,11 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
         double* L = &out.lin[(((size_t)k * G + cta) * W + w) * KBC * 32];
         for (int e = 0; e < len1; ++e) L[e] = inv[(size_t)r1 * B + e];
         for (int e = 0; e < len2; ++e) L[len1 + e] = inv[(size_t)r2 * B + e];
-        for (int h = 0; h < 2; ++h) {
-          if (!(h ? v2 : v1)) continue;
-          const int p = k0 + (h ? r2 : r1);
+      }
+      for (int i = 0; i < b; ++i) {  // phase-A rows: contiguous chunk per CTA
+        const int cta = i / (B / G), w = (i % (B / G)) / 2, h = i % 2;
+        {
+          const int p = k0 + i;
           int jn = 0, jf = 0;
           const size_t eb = (((size_t)k * G + cta) * W + w) * KA * 32;
           const size_t fb = (((size_t)k * G + cta) * W + w) * KF * 32;
@@ -143,6 +145,31 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
   for (auto& t : pool) t.join();
   if (bad) return false;
   for (double r : ratios) out.max_inv_ratio = std::max(out.max_inv_ratio, r);
+  // destinations of every solution value: the CTAs whose phase-A rows read it from the ring
+  out.xmask.assign((size_t)npan * B, 0);
+  out.xcnt.assign((size_t)(npan + 1) * G, 0);
+  const int chunk = B / G;
+  for (int p = 0; p < n; ++p) {
+    const int k0 = (p / B) * B;
+    const unsigned short bit = (unsigned short)(1u << ((p - k0) / chunk));
+    for_entries(p, [&](int q, double) {
+      if (q < k0 && q >= k0 - R) out.xmask[q] |= bit;
+    });
+  }
+  // every CTA receives at least one value of every panel: the kernel's ordering
+  // argument (panel.cu) needs "sending r(t+2) implies having received x(t+1)"
+  for (int k = 0; k < npan; ++k) {
+    unsigned short any = 0;
+    const int k0 = k * B, b = std::min(B, n - k0);
+    for (int i = 0; i < b; ++i) any |= out.xmask[k0 + i];
+    out.xmask[k0 + b - 1] |= (unsigned short)(~any & ((1u << G) - 1));
+  }
+  for (int q = 0; q < n; ++q)
+    for (int d = 0; d < G; ++d)
+      if (out.xmask[q] >> d & 1) {
+        ++out.xcnt[(size_t)(q / B) * G + d];
+        ++out.x_messages;
+      }
   return true;
 }
 

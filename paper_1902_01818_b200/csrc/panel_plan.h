@@ -18,11 +18,15 @@
 // warp q / G.  Per panel and CTA the planner emits
 //   lin [W][KBC][32]    inverse rows of the warp's pair, concatenated (row q then
 //                       row b-1-q), entry e at chunk e/32, lane e%32, zero padded;
-//   ev/ec [W][KA][32]   off-panel coefficients with ring slots (position & (R-1)),
-//                       lanes 0-15 row q, lanes 16-31 row b-1-q, entry j at
-//                       slot j/16, lane j%16;
+//   ev/ec [W][KA][32]   off-panel coefficients with ring slots (position & (R-1)) of
+//                       the CTA's phase-A rows: CTA s owns the contiguous rows
+//                       [s*B/G, (s+1)*B/G), warp w half h row s*B/G + 2w + h; entry j
+//                       at slot j/16, lane h*16 + j%16;
 //   fv/fc [W][KF][32]   off-panel coefficients older than the ring (position < kB-R),
-//                       read from the global position-ordered solution.
+//                       read from the global position-ordered solution;
+//   xmask [npan*B]      CTAs whose phase-A rows read position p from the ring (bit d =
+//                       CTA d): c_p is sent only there;
+//   xcnt [npan][G]      values of panel k each CTA receives (its mbarrier byte count / 8).
 #pragma once
 #include <vector>
 
@@ -40,6 +44,9 @@ struct PanelPlanHost {
   std::vector<int> ec;
   std::vector<double> fv;    // [npan + 1][G][W][KF][32] (last panel: zero pad)
   std::vector<int> fc;
+  std::vector<unsigned short> xmask;  // [npan * B]
+  std::vector<int> xcnt;              // [npan + 1][G]
+  long long x_messages = 0;           // sum of popcount(xmask)
 };
 
 // Dependencies of row r: entries [ptr[r], dpos[r]) (lower) or (dpos[r], ptr[r+1])

@@ -182,3 +182,49 @@ def test_gs_cluster_path_matches_oracle():
         assert rel(solver.ctx.op("gs_fwd", level, x, n), orc.gs_forward(level, x)) <= 1e-12
         assert rel(solver.ctx.op("gs_bwd", level, x, n), orc.gs_backward(level, x)) <= 1e-12
     solver.close()
+
+
+STRESS_CASES = [("cfg2", {}), ("cfg3", {"levels": 3}), ("cfg4", {"p": 4, "levels": 3}), ("cfg5", {"levels": 2})]
+
+
+@pytest.mark.parametrize("cfg,kw", STRESS_CASES)
+def test_gs_sweeps_repeatable_and_match_oracle(cfg, kw):
+    """Every level's forward/backward sweep, 12 repetitions each: bitwise identical results
+    (the panel sweep's cluster exchanges are race-free and its reductions fixed-order) and
+    within 1e-12 of SuperLU on tril/triu."""
+    pr, setup, f, solver, orc = device_solver(cfg, **kw)
+    rng = np.random.default_rng(17)
+    for level in range(1, solver.finest + 1):
+        if orc.gs[level] is None:
+            continue
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for op, ref in (("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward)):
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(11):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (cfg, level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (cfg, level, op)
+
+
+def test_level_set_engine_still_matches_oracle():
+    """IGB_GS_ENGINE=levels: the level-set sweep (used when panels do not pay off)."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup("cfg2", levels=3)
+    os.environ["IGB_GS_ENGINE"] = "levels"
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_GS_ENGINE"]
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(3)
+    for level in (1, 2, 3):
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        assert rel(solver.ctx.op("gs_fwd", level, x, n), orc.gs_forward(level, x)) <= 1e-12
+        assert rel(solver.ctx.op("gs_bwd", level, x, n), orc.gs_backward(level, x)) <= 1e-12
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    solver.close()

@@ -72,9 +72,9 @@ struct InteriorStage {
 };
 
 struct FdPlan {
-  FdSmall* d_small = nullptr;   // fused single-CTA interiors
-  int nsmall = 0, small_nmax = 0;
-  double small_bytes = 0;
+  FdCluster* d_clu = nullptr;   // fused 2-D interiors, one cluster each
+  int nclu = 0, clu_G = 1;
+  double clu_bytes = 0;
   int nsteps = 0;
   GemmDesc* d_desc[6] = {nullptr};
   int ndesc[6] = {0};
@@ -371,9 +371,9 @@ struct igb_ctx {
   void scms(int l, const double* res, double* u, bool u_zero) {
     Level& V = lev[l];
     const FdPlan& F = V.fd;
-    if (F.nsmall) {
-      launch(K_FD, F.small_bytes, [&] {
-        launch_fd_small(stream, F.d_small, F.nsmall, F.small_nmax, res, u, V.tau, u_zero ? 0 : 1);
+    if (F.nclu) {
+      launch(K_FD, F.clu_bytes, [&] {
+        launch_fd_cluster(stream, F.d_clu, F.nclu, F.clu_G, res, u, V.tau, u_zero ? 0 : 1);
       });
     }
     for (int s = 0; s < F.nsteps; ++s) {
@@ -632,24 +632,34 @@ void require_final(igb_ctx* ctx) {
 void build_fd_plan(igb_ctx* ctx, Level& V) {
   if (V.interiors.empty()) return;
   int dim = V.interiors[0].dim;
-  // small 2-D interiors: one fused CTA each; the rest: batched GEMM steps
-  std::vector<FdSmall> small;
+  // 2-D interiors up to FDC_NMAX: one fused cluster each; the rest: batched GEMM steps
+  std::vector<FdCluster> clu;
   std::vector<InteriorStage> big;
   const bool fuse = !(std::getenv("IGB_FD_FUSE") && std::string(std::getenv("IGB_FD_FUSE")) == "0");
+  int n0max = 0;
   for (auto& it : V.interiors) {
     if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
-    if (fuse && dim == 2 && it.n[0] <= FD_SMALL_NMAX && it.n[1] <= FD_SMALL_NMAX) {
-      FdSmall f{it.T[0], it.T[1], it.D, it.idx, it.n[0], it.n[1]};
-      small.push_back(f);
-      V.fd.small_nmax = std::max(V.fd.small_nmax, std::max(it.n[0], it.n[1]));
-      V.fd.small_bytes += 8.0 * (it.n[0] * it.n[0] + it.n[1] * it.n[1] + 2.0 * it.n[0] * it.n[1]) + 12.0 * it.n[0] * it.n[1];
+    if (fuse && dim == 2 && it.n[0] <= FDC_NMAX && it.n[1] <= FDC_NMAX) {
+      FdCluster f{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]};
+      clu.push_back(f);
+      n0max = std::max(n0max, it.n[0]);
+      // T0 and T1 read twice, R gathered, D, A written + read, X scattered
+      V.fd.clu_bytes += 16.0 * (it.n[0] * it.n[0] + it.n[1] * it.n[1]) + (12.0 + 8 + 16 + 12) * it.n[0] * it.n[1];
     } else {
       big.push_back(it);
     }
   }
-  if (!small.empty()) {
-    V.fd.d_small = ctx->upload(small.data(), small.size());
-    V.fd.nsmall = (int)small.size();
+  if (!clu.empty()) {
+    size_t tot = 0;
+    for (auto& f : clu) tot += (size_t)f.n0 * f.n1;
+    double* scratch = ctx->alloc<double>(tot);
+    for (auto& f : clu) {
+      f.scratch = scratch;
+      scratch += (size_t)f.n0 * f.n1;
+    }
+    V.fd.d_clu = ctx->upload(clu.data(), clu.size());
+    V.fd.nclu = (int)clu.size();
+    V.fd.clu_G = fd_cluster_size(n0max);
   }
   V.interiors = big;
   if (big.empty()) return;
@@ -764,6 +774,7 @@ int igb_create(igb_ctx** out, int device) {
     if (device < 0 || device >= count) throw ArgError("no such CUDA device");
     ctx->device = device;
     CU(cudaSetDevice(device));
+    carveout_prepare();
     CU(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
     CU(cudaEventCreate(&ctx->t0));
     CU(cudaEventCreate(&ctx->t1));

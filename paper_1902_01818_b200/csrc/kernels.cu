@@ -15,6 +15,7 @@
 //  Elementwise updates use explicit __dmul_rn/__dadd_rn so x + a*y rounds
 //  exactly like numpy's two-step evaluation (no FMA contraction).
 #include <cooperative_groups.h>
+#include <cstdlib>
 
 #include "kernels.cuh"
 
@@ -771,6 +772,32 @@ void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, do
     coarse_csc_kernel<true><<<1, threads < 32 ? 32 : threads, resident, s>>>(c, rhs, out);
   else
     coarse_csc_kernel<false><<<1, threads < 32 ? 32 : threads, base, s>>>(c, rhs, out);
+}
+
+// One shared-memory carveout for every kernel of the solve: the sweep and FD kernels
+// need (nearly) all 228 KB, and a kernel that prefers a different L1/shared split
+// forces the SM to drain and reconfigure between launches (measured: ~10 us of idle
+// per switch on small kernels).  IGB_CARVEOUT=-1 leaves the driver default.
+void carveout_prepare() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* env = std::getenv("IGB_CARVEOUT");
+  const int pct = env ? std::atoi(env) : 100;
+  if (pct < 0) return;
+  const void* funcs[] = {
+      (const void*)spmv_kernel<4>, (const void*)spmv_kernel<8>, (const void*)spmv_kernel<16>,
+      (const void*)spmv_kernel<32>, (const void*)spmv_dot_kernel<4>, (const void*)spmv_dot_kernel<8>,
+      (const void*)spmv_dot_kernel<16>, (const void*)spmv_dot_kernel<32>, (const void*)sptrsv_kernel,
+      (const void*)level_sweep_kernel<false, false>, (const void*)level_sweep_kernel<true, false>,
+      (const void*)level_sweep_kernel<false, true>, (const void*)level_sweep_kernel<true, true>,
+      (const void*)perm_gather_kernel, (const void*)perm_scatter_kernel, (const void*)coarse_csc_kernel<true>,
+      (const void*)coarse_csc_kernel<false>, (const void*)fd_gemm_kernel, (const void*)fd_small_kernel,
+      (const void*)piece_gemv_kernel, (const void*)dot_kernel, (const void*)cg_update_kernel,
+      (const void*)cg_direction_kernel, (const void*)copy_kernel, (const void*)fill_kernel};
+  for (const void* f : funcs) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  cudaGetLastError();
+  set_carveout_panel_fd(pct);
 }
 
 size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }

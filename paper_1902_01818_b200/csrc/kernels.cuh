@@ -13,6 +13,10 @@
 
 namespace igb {
 
+// Same preferred shared-memory carveout for every kernel (kernels.cu).
+void carveout_prepare();
+void set_carveout_panel_fd(int pct);   // panel.cu / fd.cu kernels
+
 // ---- CSR SpMV: y = z + sign * A x  (sign 0: y = A x) -----------------------
 void launch_spmv(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
                  const double* x, const double* z, double* y, int sign, int group);
@@ -138,6 +142,23 @@ struct FdSmall {
 constexpr int FD_SMALL_NMAX = 80;
 void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
                      double alpha, int accumulate);
+
+// ---- fused 2-D fast diagonalisation, one thread-block cluster per interior (fd.cu) --
+// n0, n1 <= FDC_NMAX; G = fd_cluster_size(max n0) CTAs of FDC_NT threads per interior;
+// scratch: n0 * n1 doubles per interior (the middle intermediate, exchanged through L2).
+constexpr int FDC_NMAX = 160;
+constexpr int FDC_NT = 160;
+struct FdCluster {
+  const double* T0;
+  const double* T1;
+  const double* D;
+  const int* idx;
+  double* scratch;
+  int n0, n1;
+};
+int fd_cluster_size(int n0max);
+void launch_fd_cluster(cudaStream_t s, const FdCluster* d_items, int nitems, int G, const double* r, double* u,
+                       double alpha, int accumulate);
 
 // ---- interface-piece dense solves (precomputed inverses) ---------------------
 struct PieceRowBlock {

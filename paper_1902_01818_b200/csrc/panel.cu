@@ -99,6 +99,8 @@ struct PanelSet {
   double lv[KL];               // inverse entries (register variant)
   double b, u0;
   int xm, xc;                  // destination mask of this lane's phase-B row; values due in bar_x
+                               // (low 16 bits) | far slots of panel t+2 (bits 16..)
+  int kf;                      // far slots in use for the next panel (fv/fc/fx)
   double ev[KA];
   int ec[KA];
   double fv[KF > 0 ? KF : 1];  // far coefficients of the NEXT panel
@@ -152,7 +154,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arm(&bar_r[0], 8u * panel_rows(0));
     if (T > 1) mbar_arm(&bar_r[1], 8u * panel_rows(1));
-    mbar_arm(bar_x, 8u * __ldg(a.xcnt + s));
+    mbar_arm(bar_x, 8u * (__ldg(a.xcnt + s) & 0xffff));
   }
   // lane hl sends to CTA hl of the cluster (G <= 16)
   const int peer = hl < G ? hl : 0;
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     for (int t = 0; t < a.pf && t < T; ++t) bulk_prefetch_l2(lin_w + t * lin_panel, 8u * KBC * 32);
 
   // set of panel t: rhs + old u + near entries of t, far entries of t+1
-  auto load = [&](Set& X, int t) {
+  auto load = [&](Set& X, int t, int kf_next) {
     const int k0 = t * B, b = panel_rows(t);
     const int ia = s * (B / G) + 2 * w + h;  // phase-A row (contiguous chunk per CTA)
     if (LREG) {
@@ -202,20 +204,26 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     }
     if (KF > 0) {
       const size_t fo = (size_t)(t + 1) * G * far_cta + far_off;  // panel npan is a zero pad
+      X.kf = kf_next;
 #pragma unroll
       for (int j = 0; j < KF; ++j) {
-        X.fv[j] = __ldg(a.fv + fo + j * 32);
-        X.fc[j] = __ldg(a.fc + fo + j * 32);
+        X.fv[j] = 0.0;
+        X.fc[j] = 0;
+        if (j < kf_next) {  // warp-uniform: most panels need at most one slot
+          X.fv[j] = __ldg(a.fv + fo + j * 32);
+          X.fc[j] = __ldg(a.fc + fo + j * 32);
+        }
       }
     }
   };
 
   Set A, Bs;
-  load(A, 0);
+  load(A, 0, KF);
 #pragma unroll
   for (int j = 0; j < (KF > 0 ? KF : 1); ++j) {
     Bs.fv[j] = 0.0;
-    Bs.fx[j] = 0.0;
+    Bs.fx[j] = 0.0;  // slots skipped by the kf test keep finite (zero or older) values
+    A.fx[j] = 0.0;
   }
   const long long t_start = clock64();
   long long tm[6] = {0, 0, 0, 0, 0, 0};
@@ -230,9 +238,9 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
 
   auto step = [&](Set& X, Set& Y, int t) {
     const int k0 = t * B, b = panel_rows(t);
-    if (t > 0) {  // x of panel t-1 complete in this CTA's ring
+    if (t > 0 && !(a.ablate & 64)) {  // x of panel t-1 complete in this CTA's ring
       mbar_wait_cluster(bar_x, (unsigned)((t - 1) & 1), 1, t - 1);
-      if (tid == 0) mbar_arm(bar_x, 8u * X.xc);
+      if (tid == 0) mbar_arm(bar_x, 8u * (X.xc & 0xffff));
     }
     mark(0);
     if (KF > 0 && t > 0 && t % far_period == 0) {
@@ -261,18 +269,20 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     sA += __shfl_xor_sync(0xffffffffu, sA, 1);
     const int rb = (t & 1) * B;
     const int ia = s * (B / G) + 2 * w + h;
-    if (ia < b && hl < G) st_async(peer_psm + 8u * (R + rb + ia), X.b - sA, peer_bar_r + 8u * (t & 1));
+    if (ia < b && hl < G && !(a.ablate & 64)) st_async(peer_psm + 8u * (R + rb + ia), X.b - sA, peer_bar_r + 8u * (t & 1));
     // issued while the residual exchange is in flight: next panel's set, old values
     if (KF > 0) {
 #pragma unroll
-      for (int j = 0; j < KF; ++j) X.fx[j] = __ldcg(a.xg + X.fc[j]);  // panel t+1: positions < tB - R + B
+      for (int j = 0; j < KF; ++j)  // panel t+1: positions < tB - R + B (final)
+        if (j < X.kf) X.fx[j] = __ldcg(a.xg + X.fc[j]);
     }
-    if (t + 1 < T) load(Y, t + 1);
+    if (t + 1 < T) load(Y, t + 1, X.xc >> 16);
     mark(2);
     // ---- phase B: inverse block, warp per row pair
-    mbar_wait_cluster(&bar_r[t & 1], (unsigned)((t >> 1) & 1), 0, t);
+    if (!(a.ablate & 64)) mbar_wait_cluster(&bar_r[t & 1], (unsigned)((t >> 1) & 1), 0, t);
+    else __syncthreads();
     if (tid == 0) {
-      if (t + 2 < T) mbar_arm(&bar_r[t & 1], 8u * panel_rows(t + 2));
+      if (t + 2 < T && !(a.ablate & 64)) mbar_arm(&bar_r[t & 1], 8u * panel_rows(t + 2));
       const int tn = t + S - 1;  // stage of panel t-1: every local warp is past it (wait_r)
       if (!LREG && !(a.ablate & 1)) {
         if (tn < T) bulk_load(lin_s + (size_t)(tn % S) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn % S]);
@@ -308,7 +318,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     }
     const double xv = h ? a2 : a1;
     if (vh) {
-      if (hl < G && (X.xm >> hl & 1)) st_async(peer_psm + 8u * ((k0 + pr) & rmask), xv, peer_bar_x);
+      if (hl < G && (X.xm >> hl & 1) && !(a.ablate & 64)) st_async(peer_psm + 8u * ((k0 + pr) & rmask), xv, peer_bar_x);
       if (hl == 0 && !(a.ablate & 32)) {
         const int p = k0 + pr;
         const int row = a.upper ? n - 1 - p : p;
@@ -323,7 +333,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     if (t + 1 < T) step(Bs, A, t + 1);
   }
   // every x of the last panel has landed here before anyone leaves the cluster
-  mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1), 1, T - 1);
+  if (!(a.ablate & 64)) mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1), 1, T - 1);
   cluster.sync();
   if (a.dbg && s == 0 && tid == 0) {
     a.dbg[0] = T;
@@ -429,6 +439,12 @@ bool panel_prepare(int G, int KBC) {
     return false;
   }
   return nclusters >= 1;
+}
+
+void set_carveout_panel(int pct) {
+  for (int kbc : {17, 9})
+    for_all_variants(kbc, [&](auto kern) { cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct); });
+  cudaGetLastError();
 }
 
 void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {

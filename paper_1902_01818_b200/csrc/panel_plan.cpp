@@ -170,6 +170,20 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
         ++out.xcnt[(size_t)(q / B) * G + d];
         ++out.x_messages;
       }
+  // bits 16..: far slots (of 16 lanes) the CTA's rows of panel k+2 use -- read by the
+  // kernel when it loads panel k+2's far entries, from the count it already holds
+  if (KF > 0) {
+    std::vector<int> slots((size_t)(npan + 2) * G, 0);
+    for (int p = 0; p < n; ++p) {
+      const int k = p / B, k0 = k * B, cta = (p - k0) / chunk;
+      int nf = 0;
+      for_entries(p, [&](int q, double) { nf += (q < k0 - R); });
+      int& sl = slots[(size_t)k * G + cta];
+      sl = std::max(sl, (nf + 15) / 16);
+    }
+    for (int k = 0; k < npan; ++k)
+      for (int d = 0; d < G; ++d) out.xcnt[(size_t)k * G + d] |= slots[(size_t)(k + 2) * G + d] << 16;
+  }
   return true;
 }
 

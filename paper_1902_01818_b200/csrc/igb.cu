@@ -136,6 +136,10 @@ struct Level {
 struct Coarse {
   bool set = false;
   int n = 0;
+  // dense operator M = P_c U^-1 L^-1 P_r (built from the same factors) for small
+  // coarse problems: one GEMV instead of 2n dependent substitution steps
+  PieceRowBlock* d_dense = nullptr;
+  int ndense = 0;
   CoarseCsc csc{};
   DevCsr L, U;
   int *Ldpos = nullptr, *Udpos = nullptr;
@@ -391,6 +395,11 @@ struct igb_ctx {
 
   void coarse_solve(const double* rhs, double* out) {
     Coarse& C = coarse;
+    if (C.ndense) {
+      const double bytes = 8.0 * C.n * (double)C.n + 24.0 * C.n;
+      launch(K_COARSE, bytes, [&] { launch_piece_gemv(stream, C.d_dense, C.ndense, rhs, out, 1.0, 0); });
+      return;
+    }
     if (C.n > 7000) {  // rhs + column pointers no longer fit in shared memory
       coarse_solve_levels(rhs, out);
       return;
@@ -1160,6 +1169,36 @@ int igb_set_coarse_lu(igb_ctx* ctx, int n0, long long l_nnz, const int* l_ptr, c
     C.csc.unnz = ucp[n0];
     C.y = ctx->alloc<double>(n0);
     C.w = ctx->alloc<double>(n0);
+    const char* ce = std::getenv("IGB_COARSE");
+    const long long dense_max = 4096;
+    if (!(ce && std::string(ce) == "csc") && n0 <= dense_max) {
+      // column j of M: the substitution of the device csc path applied to e_j
+      std::vector<double> M((size_t)n0 * n0), y(n0);
+      for (int j = 0; j < n0; ++j) {
+        std::fill(y.begin(), y.end(), 0.0);
+        y[perm_r[j]] = 1.0;  // y[k] = e_j[inv_perm_r[k]]
+        for (int c = 0; c < n0; ++c) {
+          const double yc = y[c];
+          if (yc != 0.0)
+            for (int q = lcp[c]; q < lcp[c + 1]; ++q) y[lri[q]] -= lcv[q] * yc;
+        }
+        for (int c = n0 - 1; c >= 0; --c) {
+          const double wc = y[c] / udg[c];
+          y[c] = wc;
+          if (wc != 0.0)
+            for (int q = ucp[c]; q < ucp[c + 1]; ++q) y[uri[q]] -= ucv[q] * wc;
+        }
+        for (int i = 0; i < n0; ++i) M[(size_t)i * n0 + j] = y[perm_c[i]];
+      }
+      std::vector<int> ident(n0);
+      for (int i = 0; i < n0; ++i) ident[i] = i;
+      const double* dM = ctx->upload(M.data(), M.size());
+      const int* didx = ctx->upload(ident.data(), ident.size());
+      std::vector<PieceRowBlock> blocks;
+      for (int r0 = 0; r0 < n0; r0 += 8) blocks.push_back(PieceRowBlock{dM, didx, n0, r0, std::min(8, n0 - r0)});
+      C.d_dense = ctx->upload(blocks.data(), blocks.size());
+      C.ndense = (int)blocks.size();
+    }
     C.set = true;
   });
 }
@@ -1212,7 +1251,7 @@ int igb_finalize(igb_ctx* ctx) {
     ctx->d = ctx->alloc<double>(nL);
     ctx->q = ctx->alloc<double>(nL);
     ctx->b = ctx->alloc<double>(nL);
-    ctx->partials = ctx->alloc<double>(148 * 8);
+    ctx->partials = ctx->alloc<double>(REDUCTION_MAX_BLOCKS);
     ctx->counter = ctx->alloc<unsigned>(1);
     CU(cudaMemset(ctx->counter, 0, sizeof(unsigned)));
     ctx->sc = ctx->alloc<CgScalars>(1);

@@ -719,9 +719,9 @@ inline int blocks_for(long long threads, int bs) { return (int)((threads + bs - 
 
 // ---------------------------------------------------------------------------
 int reduction_grid(int n) {
-  int g = (n + 1023) / 1024;  // >= 4 elements per thread
+  int g = (n + 255) / 256;  // one element per thread: every load in flight at once
   if (g < 1) g = 1;
-  if (g > 148 * 8) g = 148 * 8;
+  if (g > REDUCTION_MAX_BLOCKS) g = REDUCTION_MAX_BLOCKS;
   return g;
 }
 
@@ -743,7 +743,8 @@ void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, cons
                      const double* d, double* q, int group, double* partials, unsigned* counter,
                      CgScalars* sc, double* hist) {
   const int bs = 256;
-  int grid = reduction_grid(n * group / 4);
+  long long g = ((long long)n * group + bs - 1) / bs;  // one row group per thread group
+  const int grid = (int)(g < 1 ? 1 : (g > REDUCTION_MAX_BLOCKS ? REDUCTION_MAX_BLOCKS : g));
   switch (group) {
     case 4: spmv_dot_kernel<4><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
     case 8: spmv_dot_kernel<8><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;

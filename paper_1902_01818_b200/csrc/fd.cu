@@ -27,7 +27,7 @@ namespace igb {
 namespace {
 
 constexpr int FDC_RB = 10;     // rows per CTA
-constexpr int FDC_KC = 32;     // right-operand rows per chunk
+constexpr int FDC_KC = 16;     // right-operand rows per chunk
 constexpr size_t FDC_SMEM = 8 * (2 * FDC_NMAX * FDC_RB + 2 * FDC_KC * FDC_NMAX);
 
 template <class Load>
@@ -70,7 +70,7 @@ __device__ __forceinline__ void fdc_gemm(double (&acc)[FDC_RB], const double (*L
   }
 }
 
-__global__ void __launch_bounds__(FDC_NT) fd_cluster_kernel(const FdCluster* __restrict__ items, const double* r,
+__global__ void __launch_bounds__(FDC_NT, 1) fd_cluster_kernel(const FdCluster* __restrict__ items, const double* r,
                                                             double* u, double alpha, int accumulate) {
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[FDC_RB] = reinterpret_cast<double (*)[FDC_RB]>(fdc_smem);
@@ -86,11 +86,24 @@ __global__ void __launch_bounds__(FDC_NT) fd_cluster_kernel(const FdCluster* __r
   const int jj = active ? j : n1 - 1;  // idle columns load a valid dummy (never stored)
   double acc[FDC_RB];
 
+  // left-operand fill: all of a thread's loads are issued before any store (one round trip)
+  constexpr int FILL = (FDC_NMAX * FDC_RB + FDC_NT - 1) / FDC_NT;
+  auto fill = [&](bool rows) {
+    double v[FILL];
+#pragma unroll
+    for (int q = 0; q < FILL; ++q) {
+      const int e = j + q * FDC_NT, m = e / FDC_RB, i = e - m * FDC_RB;
+      const int mm = min(m, n0 - 1), ii = min(i, max(nr - 1, 0));
+      v[q] = __ldg(it.T0 + (rows ? (size_t)(r0 + ii) * n0 + mm : (size_t)mm * n0 + r0 + ii));
+    }
+#pragma unroll
+    for (int q = 0; q < FILL; ++q) {
+      const int e = j + q * FDC_NT, m = e / FDC_RB, i = e - m * FDC_RB;
+      if (m < n0) lop[m][i] = i < nr ? v[q] : 0.0;
+    }
+  };
   // 1: B = T0^T R      lop[m][i] = T0[m][r0 + i]
-  for (int e = j; e < n0 * FDC_RB; e += FDC_NT) {
-    const int m = e / FDC_RB, i = e - m * FDC_RB;
-    lop[m][i] = i < nr ? __ldg(it.T0 + (size_t)m * n0 + r0 + i) : 0.0;
-  }
+  fill(false);
   __syncthreads();
   fdc_gemm(acc, lop, n0, j, active, rch, [&](int m) { return r[__ldg(it.idx + (size_t)m * n1 + jj)]; });
 #pragma unroll
@@ -108,10 +121,10 @@ __global__ void __launch_bounds__(FDC_NT) fd_cluster_kernel(const FdCluster* __r
   }
   cluster.sync();  // every row of A written (release/acquire at cluster scope)
   // 3: B' = T0 A        lop[m][i] = T0[r0 + i][m]
-  for (int e = j; e < n0 * FDC_RB; e += FDC_NT) {
-    const int m = e / FDC_RB, i = e - m * FDC_RB;
-    lop[m][i] = i < nr ? __ldg(it.T0 + (size_t)(r0 + i) * n0 + m) : 0.0;
-  }
+  fill(true);
+  int gi[FDC_RB];  // epilogue targets, fetched two products ahead (idx -> u chain off the critical path)
+#pragma unroll
+  for (int i = 0; i < FDC_RB; ++i) gi[i] = __ldg(it.idx + (size_t)(r0 + min(i, max(nr - 1, 0))) * n1 + jj);
   __syncthreads();
   fdc_gemm(acc, lop, n0, j, active, rch, [&](int m) { return __ldcg(it.scratch + (size_t)m * n1 + jj); });
   __syncthreads();
@@ -124,9 +137,8 @@ __global__ void __launch_bounds__(FDC_NT) fd_cluster_kernel(const FdCluster* __r
 #pragma unroll
     for (int i = 0; i < FDC_RB; ++i)
       if (i < nr) {
-        const int g = __ldg(it.idx + (size_t)(r0 + i) * n1 + j);
         const double v = __dmul_rn(alpha, acc[i]);
-        u[g] = accumulate ? __dadd_rn(u[g], v) : v;
+        u[gi[i]] = accumulate ? __dadd_rn(u[gi[i]], v) : v;
       }
   }
 }

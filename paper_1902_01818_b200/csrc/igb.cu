@@ -918,12 +918,8 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   a.KA = plan.KA;
   a.KF = plan.KF;
   a.upper = dir;
-  const char* st = std::getenv("IGB_PANEL_STAGES");
-  a.stages = st ? std::max(0, std::atoi(st)) : 2;  // 0: inverse entries in registers (LREG)
-  if (a.stages == 1) a.stages = 2;
   const char* pf = std::getenv("IGB_PANEL_PF");
-  a.pf = pf ? std::max(0, std::atoi(pf)) : 2;
-  while (a.stages > 2 && panel_smem_bytes(a) > 227u * 1024) --a.stages;
+  a.pf = pf ? std::max(0, std::atoi(pf)) : 0;  // bulk L2 prefetch distance (measured: no gain)
   if (panel_smem_bytes(a) > 227u * 1024) return false;
   a.lin = ctx->upload(plan.lin.data(), plan.lin.size());
   a.ev = ctx->upload(plan.ev.data(), plan.ev.size());
@@ -948,9 +944,9 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   if (std::getenv("IGB_VERBOSE"))
     std::fprintf(stderr,
                  "[igb] level %d dir %d: panel sweep n %d depth %d panels %d (G %d B %d) KA %d KF %d near %lld far %lld "
-                 "inverse %.1f MB growth %.2f smem %zu stages %d x-messages/value %.2f\n",
+                 "inverse %.1f MB growth %.2f smem %zu x-messages/value %.2f\n",
                  level, dir, V.n, nlev, plan.npan, plan.G, plan.B, plan.KA, plan.KF, plan.near_entries,
-                 plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a), a.stages,
+                 plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a),
                  double(plan.x_messages) / V.n);
   return true;
 }

@@ -75,6 +75,7 @@ void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* x
 // See panel_plan.h: G CTAs x PANEL_W warps, panels of B = 32 G rows, inverse blocks
 // streamed by TMA, recent solution values in a DSMEM-broadcast ring of R slots.
 constexpr int PANEL_W = 16;
+constexpr int PANEL_STAGES = 2;   // TMA stages of the inverse slices (power of two)
 struct PanelArgs {
   const double* lin;  // [npan][G][W][KBC][32]
   const double* ev;   // [npan][G][W][KA][32]
@@ -87,7 +88,7 @@ struct PanelArgs {
   double* u;          // u (+)= c by row
   double* xg;         // c by position (only when KF > 0)
   int n, npan, B, R, G, KBC, KA, KF;
-  int upper, accumulate, stages, pf;
+  int upper, accumulate, pf;
   long long* dbg;     // nullable: clock64 totals of CTA 0 thread 0 (debug)
   int ablate;         // debug: bit0 no TMA, bit1 no cluster barriers, bit2 no inverse product,
                       // bit3 local stores only, bit4 no phase-A gathers,

@@ -8,7 +8,7 @@
 //            (+ entries older than the ring, gathered one panel ahead from global)
 //            -> r_i stored into every CTA's rbuf (DSMEM);   cluster barrier
 //   phase B  c_i = sum_j Tinv_kk[i][j] r_j              warp per row pair (q, b-1-q),
-//            Tinv slice of this CTA staged by a TMA bulk copy issued `stages-1`
+//            Tinv slice of this CTA staged by a TMA bulk copy issued one
 //            panels ahead -> c_i stored into every CTA's ring (DSMEM), u, xg;
 //            cluster barrier
 //
@@ -94,9 +94,8 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigne
     if (clock64() - t0 > (1LL << 31)) exchange_stuck(what, t, parity);
 }
 
-template <int KA, int KF, int KL>
+template <int KA, int KF>
 struct PanelSet {
-  double lv[KL];               // inverse entries (register variant)
   double b, u0;
   int xm, xc;                  // destination mask of this lane's phase-B row; values due in bar_x
                                // (low 16 bits) | far slots of panel t+2 (bits 16..)
@@ -123,16 +122,15 @@ struct PanelSet {
 // after every CTA sent r(t+1), i.e. after its wait_x(t): one bar_x suffices.  Old values read from global memory
 // (KF > 0) are ordered by a cluster barrier every R/B panels (a far value read
 // during panel t was written during a panel <= t - R/B).
-// LREG: the inverse slice of every warp is loaded straight into registers one panel
-// ahead (bulk L2 prefetch `pf` panels ahead) instead of TMA-staged in shared memory.
 
-template <int KBC, int KA, int KF, bool LREG>
+
+template <int KBC, int KA, int KF>
 __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs a) {
-  constexpr int KL = LREG ? KBC : 1;
-  using Set = PanelSet<KA, KF, KL>;
+  using Set = PanelSet<KA, KF>;
   extern __shared__ __align__(128) double psm[];
   constexpr int W = PANEL_W;
-  const int B = a.B, R = a.R, T = a.npan, n = a.n, S = a.stages;
+  constexpr int S = PANEL_STAGES;
+  const int B = a.B, R = a.R, T = a.npan, n = a.n;
   const cg::cluster_group cluster = cg::this_cluster();
   const int G = (int)cluster.num_blocks(), s = (int)cluster.block_rank();
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, h = l >> 4, hl = l & 15;
@@ -164,7 +162,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
 
   const double* lin_g = a.lin + (size_t)s * cta_lin;
   const size_t lin_panel = (size_t)G * cta_lin;
-  if (!LREG && tid == 0 && !(a.ablate & 1)) {
+  if (tid == 0 && !(a.ablate & 1)) {
     for (int t = 0; t < S - 1 && t < T; ++t)
       bulk_load(lin_s + (size_t)t * cta_lin, lin_g + t * lin_panel, lin_bytes, &full[t]);
     for (int t = S - 1; t < S - 1 + a.pf && t < T; ++t) bulk_prefetch_l2(lin_g + t * lin_panel, lin_bytes);
@@ -173,21 +171,12 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   const size_t ent_cta = (size_t)W * KA * 32, far_cta = (size_t)W * KF * 32;
   const size_t ent_off = ((size_t)s * W + w) * KA * 32 + l, far_off = ((size_t)s * W + w) * KF * 32 + l;
   const int rmask = R - 1;
-  const int far_period = R / B;
-  const double* lin_w = lin_g + (size_t)w * KBC * 32 + l;  // this lane's inverse entries (LREG)
-  if (LREG && l == 0 && !(a.ablate & 1))
-    for (int t = 0; t < a.pf && t < T; ++t) bulk_prefetch_l2(lin_w + t * lin_panel, 8u * KBC * 32);
+  const int far_mask = R / B - 1;  // R, B powers of two
 
   // set of panel t: rhs + old u + near entries of t, far entries of t+1
   auto load = [&](Set& X, int t, int kf_next) {
     const int k0 = t * B, b = panel_rows(t);
     const int ia = s * (B / G) + 2 * w + h;  // phase-A row (contiguous chunk per CTA)
-    if (LREG) {
-      const double* lp = lin_w + t * lin_panel;
-#pragma unroll
-      for (int c = 0; c < KL; ++c) X.lv[c] = __ldg(lp + c * 32);
-      if (l == 0 && !(a.ablate & 1) && t + a.pf < T) bulk_prefetch_l2(lp + a.pf * lin_panel, 8u * KBC * 32);
-    }
     const int pr = h ? b - 1 - pq : pq;
     const int p = min(k0 + max(pr, 0), n - 1);  // clamped: invalid rows load a finite dummy
     const int row = a.upper ? n - 1 - p : p;
@@ -243,7 +232,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
       if (tid == 0) mbar_arm(bar_x, 8u * (X.xc & 0xffff));
     }
     mark(0);
-    if (KF > 0 && t > 0 && t % far_period == 0) {
+    if (KF > 0 && t > 0 && (t & far_mask) == 0) {
       cluster_arrive();
       cluster_wait();
     }
@@ -284,32 +273,35 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     if (tid == 0) {
       if (t + 2 < T && !(a.ablate & 64)) mbar_arm(&bar_r[t & 1], 8u * panel_rows(t + 2));
       const int tn = t + S - 1;  // stage of panel t-1: every local warp is past it (wait_r)
-      if (!LREG && !(a.ablate & 1)) {
-        if (tn < T) bulk_load(lin_s + (size_t)(tn % S) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn % S]);
+      if (!(a.ablate & 1)) {
+        if (tn < T)
+          bulk_load(lin_s + (size_t)(tn & (S - 1)) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn & (S - 1)]);
         if (a.pf && tn + a.pf < T) bulk_prefetch_l2(lin_g + (tn + a.pf) * lin_panel, lin_bytes);
       }
     }
     mark(3);
-    if (!LREG && !(a.ablate & 1)) mbar_wait_parity(&full[t % S], (unsigned)((t / S) & 1));
+    if (!(a.ablate & 1)) mbar_wait_parity(&full[t & (S - 1)], (unsigned)((t / S) & 1));
     mark(4);
-    const double* L = lin_s + (size_t)(LREG ? 0 : t % S) * cta_lin + (size_t)w * KBC * 32 + l;
-    const double* rv = rbuf + rb;
-    const int len1 = v1 ? r1 + 1 : 0;
-    double a1 = 0.0, a2 = 0.0;
+    const double* L = lin_s + (size_t)(t & (S - 1)) * cta_lin + (size_t)w * KBC * 32 + l;
+    const double* rv = rbuf + rb + l;
+    // row r1 uses chunks [0, nc1), row r2 chunks [nc1, nc1 + nc2); both read r at column 32c + lane
+    const int nc1 = v1 ? (r1 + 32) >> 5 : 0, nc2 = v2 ? (r2 + 32) >> 5 : 0;
+    const double* L2 = L + 32 * nc1;
+    double a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
     if (a.ablate & 4) {
-      a1 = rv[l];
-      a2 = rv[l + 32];
+      a1 = rv[0];
+      a2 = rv[32];
     } else {
 #pragma unroll
-      for (int c = 0; c < KBC; ++c) {
-        const int e = c * 32 + l;
-        const bool first = e < len1;
-        const int j = min(first ? e : e - len1, B - 1);
-        const double v = LREG ? X.lv[LREG ? c : 0] : L[c * 32];
-        const double x = rv[j];
-        a1 = fma(first ? v : 0.0, x, a1);
-        a2 = fma(first ? 0.0 : v, x, a2);
+      for (int c = 0; c < KBC - 1; c += 2) {
+        const double x0 = rv[32 * c], x1 = rv[32 * c + 32];
+        if (c < nc1) a1 = fma(L[32 * c], x0, a1);
+        if (c + 1 < nc1) a3 = fma(L[32 * c + 32], x1, a3);
+        if (c < nc2) a2 = fma(L2[32 * c], x0, a2);
+        if (c + 1 < nc2) a4 = fma(L2[32 * c + 32], x1, a4);
       }
+      a1 += a3;
+      a2 += a4;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -344,7 +336,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
 
 template <int KBC, int KA, int KF>
 void launch_one(cudaStream_t st, const PanelArgs& a) {
-  auto kern = a.stages == 0 ? panel_sweep_kernel<KBC, KA, KF, true> : panel_sweep_kernel<KBC, KA, KF, false>;
+  auto kern = panel_sweep_kernel<KBC, KA, KF>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.G, 1, 1);
   cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
@@ -383,12 +375,9 @@ template <class F>
 void for_all_variants(int KBC, F&& f) {
   auto per_ka = [&](auto kbc, auto ka) {
     constexpr int C = decltype(kbc)::value, K = decltype(ka)::value;
-    f(panel_sweep_kernel<C, K, 0, false>);
-    f(panel_sweep_kernel<C, K, 1, false>);
-    f(panel_sweep_kernel<C, K, 4, false>);
-    f(panel_sweep_kernel<C, K, 0, true>);
-    f(panel_sweep_kernel<C, K, 1, true>);
-    f(panel_sweep_kernel<C, K, 4, true>);
+    f(panel_sweep_kernel<C, K, 0>);
+    f(panel_sweep_kernel<C, K, 1>);
+    f(panel_sweep_kernel<C, K, 4>);
   };
   auto per_kbc = [&](auto kbc) {
     per_ka(kbc, std::integral_constant<int, 2>{});
@@ -403,7 +392,7 @@ void for_all_variants(int KBC, F&& f) {
 }  // namespace
 
 size_t panel_smem_bytes(const PanelArgs& a) {
-  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)a.stages * PANEL_W * a.KBC * 32) + 8 * ((size_t)a.stages + 3);
+  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)PANEL_STAGES * PANEL_W * a.KBC * 32) + 8 * ((size_t)PANEL_STAGES + 3);
 }
 
 bool panel_prepare(int G, int KBC) {
@@ -432,8 +421,8 @@ bool panel_prepare(int G, int KBC) {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int nclusters = 0;
-  cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 0, false>, &cfg)
-                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 0, false>, &cfg);
+  cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 0>, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 0>, &cfg);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return false;

@@ -109,9 +109,11 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
         const int r1 = pq, r2 = b - 1 - pq;
         const bool v1 = pq < (b + 1) / 2, v2 = pq < b / 2;
         const int len1 = v1 ? r1 + 1 : 0, len2 = v2 ? r2 + 1 : 0;
+        // row r1's chunks (column j = 32c + lane), then row r2's, each zero padded to whole chunks
         double* L = &out.lin[(((size_t)k * G + cta) * W + w) * KBC * 32];
+        const int nc1 = (len1 + 31) / 32;
         for (int e = 0; e < len1; ++e) L[e] = inv[(size_t)r1 * B + e];
-        for (int e = 0; e < len2; ++e) L[len1 + e] = inv[(size_t)r2 * B + e];
+        for (int e = 0; e < len2; ++e) L[32 * nc1 + e] = inv[(size_t)r2 * B + e];
       }
       for (int i = 0; i < b; ++i) {  // phase-A rows: contiguous chunk per CTA
         const int cta = i / (B / G), w = (i % (B / G)) / 2, h = i % 2;

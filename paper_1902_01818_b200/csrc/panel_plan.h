@@ -16,8 +16,9 @@
 // Device work split (G CTAs of W = B/(2G) warps): panel rows are paired
 // (q, b-1-q) so every pair owns b+1 inverse entries; pair q belongs to CTA q % G,
 // warp q / G.  Per panel and CTA the planner emits
-//   lin [W][KBC][32]    inverse rows of the warp's pair, concatenated (row q then
-//                       row b-1-q), entry e at chunk e/32, lane e%32, zero padded;
+//   lin [W][KBC][32]    inverse rows of the warp's pair: row q's entries at chunks
+//                       0..nc1-1 (column 32c + lane), then row b-1-q's at chunks
+//                       nc1.. (column 32(c - nc1) + lane), zero padded; nc1 + nc2 <= KBC;
 //   ev/ec [W][KA][32]   off-panel coefficients with ring slots (position & (R-1)) of
 //                       the CTA's phase-A rows: CTA s owns the contiguous rows
 //                       [s*B/G, (s+1)*B/G), warp w half h row s*B/G + 2w + h; entry j

@@ -304,7 +304,10 @@ struct igb_ctx {
         const char* ab = std::getenv("IGB_GS_ABLATE");
         a.ablate = ab ? std::atoi(ab) : 0;
       }
-      const double bytes = Pn.lin_bytes + Pn.ent_bytes + 8.0 * V.n * (u_zero ? 2 : 3);
+      // algorithmic bytes of the triangular solve; the inverse blocks the
+      // panel sweep streams instead (Pn.lin_bytes) are an implementation choice
+      const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
       launch(K_GS, bytes, [&] { launch_panel_sweep(stream, a); });
       if (a.dbg) {
         long long hd[8];
@@ -904,7 +907,19 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   if (!force && 2 * npan > nlev) return false;
   PanelPlanHost plan;
   const int R = 8192;
-  if (!build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, R, plan))
+  // concurrent clusters (panel ranges): all of them must be co-resident
+  static int max_clu = -1;
+  if (max_clu < 0) {
+    PanelArgs probe{};
+    probe.R = R;
+    probe.B = B;
+    probe.KBC = G + 1;
+    max_clu = panel_max_clusters(G, G + 1, panel_smem_bytes(probe));
+    if (const char* ce = std::getenv("IGB_PANEL_CLUSTERS")) max_clu = std::max(1, std::min(max_clu, std::atoi(ce)));
+    max_clu = std::min(max_clu, 8);
+  }
+  if (!build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, R, max_clu,
+                        plan))
     return false;
   PanelDev& P = V.panel[dir];
   PanelArgs& a = P.args;
@@ -918,6 +933,12 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   a.KA = plan.KA;
   a.KF = plan.KF;
   a.upper = dir;
+  a.nclu = plan.nclu;
+  for (int c = 0; c <= plan.nclu; ++c) {
+    a.split[c] = plan.split[c];
+    a.rstart[c] = plan.rstart[c];
+  }
+  if (const char* h = std::getenv("IGB_PANEL_NOHINT")) a.ablate |= std::atoi(h) ? 128 : 0;
   const char* pf = std::getenv("IGB_PANEL_PF");
   a.pf = pf ? std::max(0, std::atoi(pf)) : 0;  // bulk L2 prefetch distance (measured: no gain)
   if (panel_smem_bytes(a) > 227u * 1024) return false;
@@ -929,11 +950,13 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   if (plan.KF > 0) {
     a.fv = ctx->upload(plan.fv.data(), plan.fv.size());
     a.fc = ctx->upload(plan.fc.data(), plan.fc.size());
-    if (!V.xg) {
-      V.xg = ctx->alloc<double>(V.n);
-      CU(cudaMemset(V.xg, 0, sizeof(double) * V.n));  // padded far entries read position 0
-    }
-    a.xg = V.xg;
+    // per level and direction: [2][n] copy, every entry "not produced yet" (panel.cu)
+    std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF1234ULL);
+    a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
+    int* ctr = ctx->alloc<int>(2);
+    CU(cudaMemset(ctr, 0, 2 * sizeof(int)));
+    a.par_ctr = ctr;
+    a.done_ctr = reinterpret_cast<unsigned*>(ctr + 1);
   }
   P.npan = plan.npan;
   P.near = plan.near_entries;
@@ -944,10 +967,10 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   if (std::getenv("IGB_VERBOSE"))
     std::fprintf(stderr,
                  "[igb] level %d dir %d: panel sweep n %d depth %d panels %d (G %d B %d) KA %d KF %d near %lld far %lld "
-                 "inverse %.1f MB growth %.2f smem %zu x-messages/value %.2f\n",
+                 "inverse %.1f MB growth %.2f smem %zu x-messages/value %.2f clusters %d (panel-times %.0f of %d)\n",
                  level, dir, V.n, nlev, plan.npan, plan.G, plan.B, plan.KA, plan.KF, plan.near_entries,
                  plan.far_entries, P.lin_bytes / 1e6, plan.max_inv_ratio, panel_smem_bytes(a),
-                 double(plan.x_messages) / V.n);
+                 double(plan.x_messages) / V.n, plan.nclu, plan.makespan, plan.npan);
   return true;
 }
 

@@ -86,16 +86,22 @@ struct PanelArgs {
   const int* xcnt;              // [npan+1][G] values each CTA receives per panel
   const double* res;  // right-hand side by row
   double* u;          // u (+)= c by row
-  double* xg;         // c by position (only when KF > 0)
+  double* xg;         // [2][n] c by position, halves by sweep parity (only when KF > 0)
+  int* par_ctr;       // sweep parity of this level and direction (device)
+  unsigned* done_ctr; // CTAs finished (device), reset by the last one
   int n, npan, B, R, G, KBC, KA, KF;
+  int nclu;           // clusters, one per panel range
+  int split[9];       // panel ranges: cluster c sweeps panels [split[c], split[c+1]) ...
+  int rstart[9];      // ... = positions [rstart[c], rstart[c+1]), panels of B rows from rstart[c]
   int upper, accumulate, pf;
   long long* dbg;     // nullable: clock64 totals of CTA 0 thread 0 (debug)
   int ablate;         // debug: bit0 no TMA, bit1 no cluster barriers, bit2 no inverse product,
                       // bit3 local stores only, bit4 no phase-A gathers,
-                      // bit5 no u / xg traffic
+                      // bit5 no u / xg traffic, bit7 no L2 evict-first hint on the inverse stream
 };
 size_t panel_smem_bytes(const PanelArgs& a);
 bool panel_prepare(int G, int KBC);   // false: no cluster of G CTAs fits this device
+int panel_max_clusters(int G, int KBC, size_t smem);  // clusters of G CTAs co-resident
 void launch_panel_sweep(cudaStream_t s, const PanelArgs& a);
 
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem

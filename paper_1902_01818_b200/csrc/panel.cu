@@ -32,12 +32,28 @@ __device__ __forceinline__ unsigned saddr(const void* p) { return (unsigned)__cv
 __device__ __forceinline__ void mbar_init1(unsigned long long* b) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(saddr(b)) : "memory");
 }
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+// The inverse blocks are read once per sweep (147 MB per direction on cfg2's finest level, more than
+// L2): load them with an evict-first L2 policy so they do not push the matrices and vectors the
+// rest of the cycle reuses out of L2.
+__device__ __forceinline__ unsigned long long evict_first_policy() {
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long policy, bool hint) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(bar)), "r"(bytes) : "memory");
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
-      "l"(src), "r"(bytes), "r"(saddr(bar))
-      : "memory");
+  if (hint)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+            saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar)), "l"(policy)
+        : "memory");
+  else
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(saddr(dst)),
+        "l"(src), "r"(bytes), "r"(saddr(bar))
+        : "memory");
 }
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
@@ -83,8 +99,9 @@ __device__ __forceinline__ bool mbar_try(unsigned long long* b, unsigned parity)
 // Wait for a phase of an exchange mbarrier.  Watchdog: a protocol error must not hang
 // the device -- after ~2^31 cycles report and trap (the launch fails with an error).
 __device__ __noinline__ void exchange_stuck(int what, int t, unsigned parity) {
-  printf("[igb panel] CTA %d thread %d: %s exchange of panel %d (parity %u) never completed\n",
-         (int)cg::this_cluster().block_rank(), (int)threadIdx.x, what ? "solution" : "residual", t, parity);
+  printf("[igb panel] cluster %d CTA %d thread %d: %s exchange of local panel %d (parity %u) never completed\n",
+         (int)(blockIdx.x / cg::this_cluster().num_blocks()), (int)cg::this_cluster().block_rank(), (int)threadIdx.x,
+         what ? "solution" : "residual", t, parity);
   __trap();
 }
 __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigned parity, int what = 0, int t = 0) {
@@ -92,6 +109,30 @@ __device__ __forceinline__ void mbar_wait_cluster(unsigned long long* b, unsigne
   const long long t0 = clock64();
   while (!mbar_try(b, parity))
     if (clock64() - t0 > (1LL << 31)) exchange_stuck(what, t, parity);
+}
+
+// Global solution copy: two halves selected by the sweep parity; a value not yet produced in
+// this sweep reads as PANEL_PENDING (a signalling NaN no arithmetic produces).  The producer
+// writes the value into the current half and PENDING into the other (ready for the next sweep
+// of this level and direction, which starts only after this kernel has finished).
+constexpr unsigned long long PANEL_PENDING = 0x7FF4DEADBEEF1234ULL;
+__device__ __forceinline__ bool pending(double v) {
+  return (unsigned long long)__double_as_longlong(v) == PANEL_PENDING;
+}
+__device__ __noinline__ void poll_stuck(int pos) {
+  printf("[igb panel] cluster %d CTA %d thread %d: solution value at position %d never produced\n",
+         (int)(blockIdx.x / cg::this_cluster().num_blocks()), (int)cg::this_cluster().block_rank(),
+         (int)threadIdx.x, pos);
+  __trap();
+}
+__device__ __forceinline__ double poll_value(const double* xg, int pos, double v) {
+  if (!pending(v)) return v;
+  const long long t0 = clock64();
+  do {
+    v = __ldcg(xg + pos);
+    if (clock64() - t0 > (1LL << 31)) poll_stuck(pos);
+  } while (pending(v));
+  return v;
 }
 
 template <int KA, int KF>
@@ -119,9 +160,12 @@ struct PanelSet {
 // CTA at least one value of every panel so this holds; hence bar_r needs two
 // parities, rbuf two buffers, and after wait_r(t) every local warp is past phase
 // B(t-1) (so the TMA stage of panel t-1 may be refilled).  x(t+1) is produced only
-// after every CTA sent r(t+1), i.e. after its wait_x(t): one bar_x suffices.  Old values read from global memory
-// (KF > 0) are ordered by a cluster barrier every R/B panels (a far value read
-// during panel t was written during a panel <= t - R/B).
+// after every CTA sent r(t+1), i.e. after its wait_x(t): one bar_x suffices.
+//
+// Clusters: cluster c sweeps panels [split[c], split[c+1]); values of earlier ranges and
+// values older than the ring come from the global copy, fetched one panel ahead and polled
+// until produced.  Dependencies point only to earlier positions, so a cluster never waits
+// for a later one.
 
 
 template <int KBC, int KA, int KF>
@@ -130,9 +174,13 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   extern __shared__ __align__(128) double psm[];
   constexpr int W = PANEL_W;
   constexpr int S = PANEL_STAGES;
-  const int B = a.B, R = a.R, T = a.npan, n = a.n;
+  const int B = a.B, R = a.R, n = a.n;
   const cg::cluster_group cluster = cg::this_cluster();
   const int G = (int)cluster.num_blocks(), s = (int)cluster.block_rank();
+  const int ci = blockIdx.x / G;
+  const int p0 = a.split[ci], p1 = a.split[ci + 1];  // this cluster's panels ...
+  const int rs = a.rstart[ci], re = a.rstart[ci + 1];  // ... cover positions [rs, re), B each from rs
+  const int T = p1 - p0;
   const int tid = threadIdx.x, w = tid >> 5, l = tid & 31, h = l >> 4, hl = l & 15;
   const int pq = w * G + s;  // pair index: rows pq and b-1-pq of every panel
   double* ring = psm;
@@ -144,7 +192,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   unsigned long long* bar_x = bars + S + 2;
   const size_t cta_lin = (size_t)W * KBC * 32;
   const unsigned lin_bytes = (unsigned)(cta_lin * 8);
-  auto panel_rows = [&](int t) { return min(B, n - t * B); };
+  auto panel_rows = [&](int t) { return min(B, re - (rs + t * B)); };  // local panel index t
 
   for (int i = tid; i < R + 2 * B; i += W * 32) psm[i] = 0.0;
   if (tid == 0) {
@@ -152,7 +200,7 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     mbar_arm(&bar_r[0], 8u * panel_rows(0));
     if (T > 1) mbar_arm(&bar_r[1], 8u * panel_rows(1));
-    mbar_arm(bar_x, 8u * (__ldg(a.xcnt + s) & 0xffff));
+    mbar_arm(bar_x, 8u * (__ldg(a.xcnt + (size_t)p0 * G + s) & 0xffff));
   }
   // lane hl sends to CTA hl of the cluster (G <= 16)
   const int peer = hl < G ? hl : 0;
@@ -160,22 +208,27 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   const unsigned peer_bar_r = mapa(saddr(bar_r), peer), peer_bar_x = mapa(saddr(bar_x), peer);  // + 8 (t & 1)
   cluster.sync();
 
-  const double* lin_g = a.lin + (size_t)s * cta_lin;
+  const double* lin_g = a.lin + ((size_t)p0 * G + s) * cta_lin;  // panel p0 of this CTA
+  const unsigned long long l2pol = evict_first_policy();
+  const bool hint = !(a.ablate & 128);
   const size_t lin_panel = (size_t)G * cta_lin;
   if (tid == 0 && !(a.ablate & 1)) {
     for (int t = 0; t < S - 1 && t < T; ++t)
-      bulk_load(lin_s + (size_t)t * cta_lin, lin_g + t * lin_panel, lin_bytes, &full[t]);
+      bulk_load(lin_s + (size_t)t * cta_lin, lin_g + t * lin_panel, lin_bytes, &full[t], l2pol, hint);
     for (int t = S - 1; t < S - 1 + a.pf && t < T; ++t) bulk_prefetch_l2(lin_g + t * lin_panel, lin_bytes);
   }
 
   const size_t ent_cta = (size_t)W * KA * 32, far_cta = (size_t)W * KF * 32;
   const size_t ent_off = ((size_t)s * W + w) * KA * 32 + l, far_off = ((size_t)s * W + w) * KF * 32 + l;
   const int rmask = R - 1;
-  const int far_mask = R / B - 1;  // R, B powers of two
+  const int par = KF > 0 ? *a.par_ctr : 0;  // sweep parity: stable for the whole launch
+  const double* xg_cur = a.xg + (size_t)par * n;
+  double* xg_set = a.xg + (size_t)par * n;
+  double* xg_clr = a.xg + (size_t)(par ^ 1) * n;
 
-  // set of panel t: rhs + old u + near entries of t, far entries of t+1
+  // set of local panel t: rhs + old u + near entries of t, far entries of t+1
   auto load = [&](Set& X, int t, int kf_next) {
-    const int k0 = t * B, b = panel_rows(t);
+    const int k = p0 + t, k0 = rs + t * B, b = panel_rows(t);
     const int ia = s * (B / G) + 2 * w + h;  // phase-A row (contiguous chunk per CTA)
     const int pr = h ? b - 1 - pq : pq;
     const int p = min(k0 + max(pr, 0), n - 1);  // clamped: invalid rows load a finite dummy
@@ -184,20 +237,21 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     X.b = __ldg(a.res + (a.upper ? n - 1 - pa : pa));
     if (a.accumulate) X.u0 = a.u[row];
     X.xm = __ldg(a.xmask + p);
-    X.xc = __ldg(a.xcnt + (size_t)t * G + s);
-    const size_t eo = (size_t)t * G * ent_cta + ent_off;
+    X.xc = __ldg(a.xcnt + (size_t)k * G + s);
+    const size_t eo = (size_t)k * G * ent_cta + ent_off;
 #pragma unroll
     for (int j = 0; j < KA; ++j) {
       X.ev[j] = __ldg(a.ev + eo + j * 32);
       X.ec[j] = __ldg(a.ec + eo + j * 32);
     }
     if (KF > 0) {
-      const size_t fo = (size_t)(t + 1) * G * far_cta + far_off;  // panel npan is a zero pad
+      const int kn = k + 1 < p1 ? k + 1 : a.npan;  // panel npan is a zero pad
+      const size_t fo = (size_t)kn * G * far_cta + far_off;
       X.kf = kf_next;
 #pragma unroll
       for (int j = 0; j < KF; ++j) {
         X.fv[j] = 0.0;
-        X.fc[j] = 0;
+        X.fc[j] = -1;
         if (j < kf_next) {  // warp-uniform: most panels need at most one slot
           X.fv[j] = __ldg(a.fv + fo + j * 32);
           X.fc[j] = __ldg(a.fc + fo + j * 32);
@@ -214,6 +268,17 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     Bs.fx[j] = 0.0;  // slots skipped by the kf test keep finite (zero or older) values
     A.fx[j] = 0.0;
   }
+  Bs.kf = 0;
+  if (KF > 0) {  // the range's first panel: its far entries (other ranges) belong to no earlier set
+    const size_t fo = (size_t)p0 * G * far_cta + far_off;
+    Bs.kf = KF;
+#pragma unroll
+    for (int j = 0; j < KF; ++j) {
+      Bs.fv[j] = __ldg(a.fv + fo + j * 32);
+      Bs.fc[j] = __ldg(a.fc + fo + j * 32);
+      if (Bs.fc[j] >= 0) Bs.fx[j] = __ldcg(xg_cur + Bs.fc[j]);
+    }
+  }
   const long long t_start = clock64();
   long long tm[6] = {0, 0, 0, 0, 0, 0};
   long long tprev = t_start;
@@ -226,21 +291,20 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   };
 
   auto step = [&](Set& X, Set& Y, int t) {
-    const int k0 = t * B, b = panel_rows(t);
+    const int k0 = rs + t * B, b = panel_rows(t);
     if (t > 0 && !(a.ablate & 64)) {  // x of panel t-1 complete in this CTA's ring
       mbar_wait_cluster(bar_x, (unsigned)((t - 1) & 1), 1, t - 1);
       if (tid == 0) mbar_arm(bar_x, 8u * (X.xc & 0xffff));
     }
     mark(0);
-    if (KF > 0 && t > 0 && (t & far_mask) == 0) {
-      cluster_arrive();
-      cluster_wait();
-    }
-    // far part of panel t (values gathered during panel t-1)
+    // far part of panel t (values gathered during panel t-1; re-polled if not produced yet)
     double sA = 0.0;
     if (KF > 0) {
 #pragma unroll
-      for (int j = 0; j < KF; ++j) sA = fma(Y.fv[j], Y.fx[j], sA);
+      for (int j = 0; j < KF; ++j) {
+        if (j < Y.kf && Y.fc[j] >= 0) Y.fx[j] = poll_value(xg_cur, Y.fc[j], Y.fx[j]);
+        sA = fma(Y.fv[j], Y.fx[j], sA);
+      }
     }
     mark(1);
     // ---- phase A: off-panel part, half-warp per row
@@ -263,7 +327,10 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
     if (KF > 0) {
 #pragma unroll
       for (int j = 0; j < KF; ++j)  // panel t+1: positions < tB - R + B (final)
-        if (j < X.kf) X.fx[j] = __ldcg(a.xg + X.fc[j]);
+        if (j < X.kf) {  // padded slots (fc < 0) hold 0: never PENDING times a zero coefficient
+          if (X.fc[j] >= 0) X.fx[j] = __ldcg(xg_cur + X.fc[j]);
+          else X.fx[j] = 0.0;
+        }
     }
     if (t + 1 < T) load(Y, t + 1, X.xc >> 16);
     mark(2);
@@ -275,7 +342,8 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
       const int tn = t + S - 1;  // stage of panel t-1: every local warp is past it (wait_r)
       if (!(a.ablate & 1)) {
         if (tn < T)
-          bulk_load(lin_s + (size_t)(tn & (S - 1)) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn & (S - 1)]);
+          bulk_load(lin_s + (size_t)(tn & (S - 1)) * cta_lin, lin_g + tn * lin_panel, lin_bytes, &full[tn & (S - 1)],
+                    l2pol, hint);
         if (a.pf && tn + a.pf < T) bulk_prefetch_l2(lin_g + (tn + a.pf) * lin_panel, lin_bytes);
       }
     }
@@ -315,7 +383,10 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
         const int p = k0 + pr;
         const int row = a.upper ? n - 1 - p : p;
         a.u[row] = a.accumulate ? X.u0 + xv : xv;
-        if (KF > 0) __stcg(a.xg + p, xv);
+        if (KF > 0) {
+          __stcg(xg_set + p, xv);
+          __stcg(xg_clr + p, __longlong_as_double((long long)PANEL_PENDING));
+        }
       }
     }
     mark(5);
@@ -327,6 +398,14 @@ __global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs 
   // every x of the last panel has landed here before anyone leaves the cluster
   if (!(a.ablate & 64)) mbar_wait_cluster(bar_x, (unsigned)((T - 1) & 1), 1, T - 1);
   cluster.sync();
+  if (KF > 0 && tid == 0) {  // the last CTA of the grid flips the parity for the next sweep
+    __threadfence();
+    if (atomicAdd(a.done_ctr, 1u) == gridDim.x - 1) {
+      *a.done_ctr = 0u;
+      *a.par_ctr = par ^ 1;
+      __threadfence();
+    }
+  }
   if (a.dbg && s == 0 && tid == 0) {
     a.dbg[0] = T;
     a.dbg[1] = clock64() - t_start;
@@ -338,7 +417,7 @@ template <int KBC, int KA, int KF>
 void launch_one(cudaStream_t st, const PanelArgs& a) {
   auto kern = panel_sweep_kernel<KBC, KA, KF>;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(a.G, 1, 1);
+  cfg.gridDim = dim3(a.G * a.nclu, 1, 1);
   cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
   cfg.dynamicSmemBytes = panel_smem_bytes(a);
   cfg.stream = st;
@@ -434,6 +513,28 @@ void set_carveout_panel(int pct) {
   for (int kbc : {17, 9})
     for_all_variants(kbc, [&](auto kern) { cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct); });
   cudaGetLastError();
+}
+
+int panel_max_clusters(int G, int KBC, size_t smem) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(G * 8, 1, 1);
+  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = G;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int nclusters = 0;
+  cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 4>, &cfg)
+                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 4>, &cfg);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 1;
+  }
+  return nclusters < 1 ? 1 : nclusters;
 }
 
 void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {

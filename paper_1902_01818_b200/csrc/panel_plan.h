@@ -23,11 +23,19 @@
 //                       the CTA's phase-A rows: CTA s owns the contiguous rows
 //                       [s*B/G, (s+1)*B/G), warp w half h row s*B/G + 2w + h; entry j
 //                       at slot j/16, lane h*16 + j%16;
-//   fv/fc [W][KF][32]   off-panel coefficients older than the ring (position < kB-R),
-//                       read from the global position-ordered solution;
+//   fv/fc [W][KF][32]   off-panel coefficients outside the ring: older than kB-R, or in an
+//                       earlier range (another cluster) -- read from the global
+//                       position-ordered solution, polled until it holds this sweep's value;
 //   xmask [npan*B]      CTAs whose phase-A rows read position p from the ring (bit d =
 //                       CTA d): c_p is sent only there;
 //   xcnt [npan][G]      values of panel k each CTA receives (its mbarrier byte count / 8).
+//
+// Ranges: the panels are split into nclu contiguous ranges, one thread-block cluster each,
+// running concurrently.  A range depends on earlier ranges only through global values, so
+// e.g. the second of two side-by-side patches lags the first by a few grid lines instead of
+// waiting for it.  Range starts are rows whose nearest earlier dependency lies >= 2B back
+// (patch starts in patch-wise numberings), added greedily while a simulation of panel
+// completion times improves (panel_plan.cpp).
 #pragma once
 #include <vector>
 
@@ -38,6 +46,11 @@ struct PanelPlanHost {
   int B = 512, G = 16, W = 16, R = 8192;
   int KBC = 17, KA = 0, KF = 0;
   int npan = 0;
+  int nclu = 1;                      // clusters (ranges)
+  std::vector<int> split;            // nclu + 1 panel indices, split[0] = 0, split[nclu] = npan
+  std::vector<int> rstart;           // nclu + 1 positions: range c = [rstart[c], rstart[c+1]); its
+                                     // panels start at rstart[c] + j B
+  double makespan = 0;               // simulated panel-times of the chosen ranges (nclu = 1: npan)
   long long near_entries = 0, far_entries = 0;
   double max_inv_ratio = 0;  // max_k |T_kk^-1|_max * |T_kk|_max (growth diagnostic)
   std::vector<double> lin;   // [npan][G][W][KBC][32]
@@ -54,6 +67,6 @@ struct PanelPlanHost {
 // (upper), diagonal val[dpos[r]].  Returns false when a row has more off-panel
 // entries than the kernel variants cover (KA > 12 or KF > 4).
 bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos,
-                      bool upper, int G, int R, PanelPlanHost& out);
+                      bool upper, int G, int R, int max_clusters, PanelPlanHost& out);
 
 }  // namespace igb

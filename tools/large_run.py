@@ -1,6 +1,6 @@
 """Full-size runs: host setup, device PCG (timed), CPU oracle PCG (timed), parity summary.
 
-python tools/large_run.py cfg5 [cfg4:p=8 ...]  ->  one JSON line per configuration
+python tools/large_run.py cfg5 [cfg4:p=8:nooracle ...]  ->  JSON lines per configuration
 """
 import json
 import os
@@ -16,8 +16,10 @@ sys.path.insert(0, ROOT)
 from paper_1902_01818_b200 import configs, multigrid  # noqa: E402
 
 
-def run(spec, with_oracle=True):
+def run(spec):
     name, *opts = spec.split(":")
+    with_oracle = "nooracle" not in opts
+    opts = [o for o in opts if o != "nooracle"]
     kw = {k: int(v) for k, v in (o.split("=") for o in opts)}
     out = {"cfg": spec}
     t = time.perf_counter()

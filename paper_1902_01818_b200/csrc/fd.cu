@@ -1,40 +1,43 @@
-// fd.cu -- fused 2-D fast diagonalisation on a thread-block cluster (sm_100a).
+// fd.cu -- fused 2-D fast diagonalisation (sm_100a).
 //
 // SCMS interior solve (smoothers.py:272-301, square-transform form of
 // ScmsInteriorSolver): X = T0 ((T0^T R T1) ./ D) T1^T with R = r[idx], and
-// u[idx] (+)= alpha X.  One cluster of G CTAs per interior; CTA c owns the rows
-// [c rb, c rb + rb) (rb <= FDC_RB) of every intermediate, thread j owns column j:
+// u[idx] (+)= alpha X.  Two launches per SCMS application, split where rows of the
+// middle intermediate are exchanged:
 //
-//   1  B  = T0^T R          left T0[:, rows]^T   right R (gathered from r)
-//   2  A  = (B T1) ./ D     left B (own rows)    right T1          -> A rows to scratch
-//      cluster barrier (A complete in L2)
-//   3  B' = T0 A            left T0[rows, :]     right A (scratch)
-//   4  X  = B' T1^T         left B' (own rows)   right T1^T        -> u[idx] (+)= alpha X
+//   fd_front   1  B  = T0^T R          left T0[:, rows]^T   right R (gathered from r)
+//              2  A  = (B T1) ./ D     left B (own rows)    right T1      -> rows of A to scratch
+//   fd_back    3  B' = T0 A            left T0[rows, :]     right A (scratch, L2)
+//              4  X  = B' T1^T         left B' (own rows)   right T1^T    -> u[idx] (+)= alpha X
 //
-// Left operands live in shared memory as [m][i] (a 10-double row per m: one
-// broadcast load feeds 10 FMAs of the thread's column); right operands stream
-// through a double-buffered [FDC_KC][FDC_NMAX] shared chunk, loaded into
+// Every CTA owns RB rows of one interior (all interiors of a level in one grid, ~2 CTAs
+// per SM) and thread j owns column j.  Left operands live in shared memory as [m][i] (RB
+// doubles per m: broadcast loads feeding RB FMAs of the thread's column); right operands
+// stream through a double-buffered [FDC_KC][FDC_NMAX] shared chunk, loaded into
 // registers one chunk ahead.
-#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
-
-namespace cg = cooperative_groups;
 
 namespace igb {
 
 namespace {
 
-constexpr int FDC_RB = 10;     // rows per CTA
-constexpr int FDC_KC = 16;     // right-operand rows per chunk
-constexpr size_t FDC_SMEM = 8 * (2 * FDC_NMAX * FDC_RB + 2 * FDC_KC * FDC_NMAX);
+constexpr int FDC_KC = 16;  // right-operand rows per chunk
 
-template <class Load>
-__device__ __forceinline__ void fdc_gemm(double (&acc)[FDC_RB], const double (*L)[FDC_RB], int K, int j, bool active,
+template <int RB>
+constexpr size_t fd_smem() {
+  return 8 * (2 * (size_t)FDC_NMAX * RB + 2 * (size_t)FDC_KC * FDC_NMAX);
+}
+
+// acc[i] = sum_m L[m][i] * Rt(m, j) for m < K; the right operand streams through two shared
+// chunks, each thread loading its column of the next chunk into registers while the
+// current one is multiplied.
+template <int RB, class Load>
+__device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB], int K, int j,
                                          double (*rch)[FDC_KC][FDC_NMAX], Load ld) {
 #pragma unroll
-  for (int i = 0; i < FDC_RB; ++i) acc[i] = 0.0;
+  for (int i = 0; i < RB; ++i) acc[i] = 0.0;
   double pre[FDC_KC];
 #pragma unroll
   for (int k = 0; k < FDC_KC; ++k) pre[k] = ld(min(k, K - 1));  // clamped rows are never consumed
@@ -52,131 +55,164 @@ __device__ __forceinline__ void fdc_gemm(double (&acc)[FDC_RB], const double (*L
     const int m0 = q * FDC_KC;
     const int kn = min(FDC_KC, K - m0);
     if (kn == FDC_KC) {
-#pragma unroll 8
+#pragma unroll
       for (int k = 0; k < FDC_KC; ++k) {
         const double x = buf[k][j];
         const double* l = L[m0 + k];
 #pragma unroll
-        for (int i = 0; i < FDC_RB; ++i) acc[i] = fma(l[i], x, acc[i]);
+        for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], x, acc[i]);
       }
     } else {
       for (int k = 0; k < kn; ++k) {
         const double x = buf[k][j];
         const double* l = L[m0 + k];
 #pragma unroll
-        for (int i = 0; i < FDC_RB; ++i) acc[i] = fma(l[i], x, acc[i]);
+        for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], x, acc[i]);
       }
     }
   }
 }
 
-__global__ void __launch_bounds__(FDC_NT, 1) fd_cluster_kernel(const FdCluster* __restrict__ items, const double* r,
-                                                            double* u, double alpha, int accumulate) {
-  extern __shared__ __align__(16) double fdc_smem[];
-  double (*lop)[FDC_RB] = reinterpret_cast<double (*)[FDC_RB]>(fdc_smem);
-  double (*outT)[FDC_RB] = lop + FDC_NMAX;
-  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(fdc_smem + 2 * FDC_NMAX * FDC_RB);
-  const cg::cluster_group cluster = cg::this_cluster();
-  const int G = (int)cluster.num_blocks(), c = (int)cluster.block_rank();
-  const FdCluster it = items[blockIdx.x / G];
-  const int n0 = it.n0, n1 = it.n1;
-  const int rb = (n0 + G - 1) / G, r0 = c * rb, nr = max(0, min(rb, n0 - r0));
-  const int j = threadIdx.x;
-  const bool active = j < n1;
-  const int jj = active ? j : n1 - 1;  // idle columns load a valid dummy (never stored)
-  double acc[FDC_RB];
+struct FdCtx {
+  FdCluster it;
+  int r0, nr, n0, n1, j, jj;
+  bool active;
+};
 
-  // left-operand fill: all of a thread's loads are issued before any store (one round trip)
-  constexpr int FILL = (FDC_NMAX * FDC_RB + FDC_NT - 1) / FDC_NT;
-  auto fill = [&](bool rows) {
-    double v[FILL];
+__device__ __forceinline__ FdCtx fd_locate(const FdBatch& bt) {
+  FdCtx c;
+  int item = 0;
+#pragma unroll 1
+  for (int i = 1; i < bt.nitems; ++i)
+    if ((int)blockIdx.x >= bt.cta0[i]) item = i;
+  c.it = bt.items[item];
+  c.n0 = c.it.n0;
+  c.n1 = c.it.n1;
+  c.r0 = ((int)blockIdx.x - bt.cta0[item]) * bt.rb;
+  c.nr = max(0, min(bt.rb, c.n0 - c.r0));
+  c.j = threadIdx.x;
+  c.active = c.j < c.n1;
+  c.jj = c.active ? c.j : c.n1 - 1;  // idle columns load a valid dummy (never stored)
+  return c;
+}
+
+// left-operand fill: lop[m][i] = T0[m][r0+i] (cols) or T0[r0+i][m] (rows); every load of a
+// thread is issued before its stores (one round trip)
+template <int RB>
+__device__ __forceinline__ void fd_fill(double (*lop)[RB], const FdCtx& c, bool rows) {
+  constexpr int FILL = (FDC_NMAX * RB + FDC_NT - 1) / FDC_NT;
+  double v[FILL];
 #pragma unroll
-    for (int q = 0; q < FILL; ++q) {
-      const int e = j + q * FDC_NT, m = e / FDC_RB, i = e - m * FDC_RB;
-      const int mm = min(m, n0 - 1), ii = min(i, max(nr - 1, 0));
-      v[q] = __ldg(it.T0 + (rows ? (size_t)(r0 + ii) * n0 + mm : (size_t)mm * n0 + r0 + ii));
-    }
+  for (int q = 0; q < FILL; ++q) {
+    const int e = c.j + q * FDC_NT, m = e / RB, i = e - m * RB;
+    const int mm = min(m, c.n0 - 1), ii = min(i, max(c.nr - 1, 0));
+    v[q] = __ldg(c.it.T0 + (rows ? (size_t)(c.r0 + ii) * c.n0 + mm : (size_t)mm * c.n0 + c.r0 + ii));
+  }
 #pragma unroll
-    for (int q = 0; q < FILL; ++q) {
-      const int e = j + q * FDC_NT, m = e / FDC_RB, i = e - m * FDC_RB;
-      if (m < n0) lop[m][i] = i < nr ? v[q] : 0.0;
-    }
-  };
-  // 1: B = T0^T R      lop[m][i] = T0[m][r0 + i]
-  fill(false);
+  for (int q = 0; q < FILL; ++q) {
+    const int e = c.j + q * FDC_NT, m = e / RB, i = e - m * RB;
+    if (m < c.n0) lop[m][i] = i < c.nr ? v[q] : 0.0;
+  }
+}
+
+template <int RB>
+__global__ void __launch_bounds__(FDC_NT, 2) fd_front_kernel(const __grid_constant__ FdBatch bt, const double* r) {
+  extern __shared__ __align__(16) double fdc_smem[];
+  double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
+  double (*outT)[RB] = lop + FDC_NMAX;
+  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(fdc_smem + 2 * FDC_NMAX * RB);
+  const FdCtx c = fd_locate(bt);
+  const int n1 = c.n1, jj = c.jj;
+  double acc[RB];
+  // 1: B = T0^T R
+  fd_fill<RB>(lop, c, false);
   __syncthreads();
-  fdc_gemm(acc, lop, n0, j, active, rch, [&](int m) { return r[__ldg(it.idx + (size_t)m * n1 + jj)]; });
+  fdc_gemm<RB>(acc, lop, c.n0, c.j, rch, [&](int m) { return r[__ldg(c.it.idx + (size_t)m * n1 + jj)]; });
 #pragma unroll
-  for (int i = 0; i < FDC_RB; ++i) outT[j][i] = acc[i];
+  for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
   __syncthreads();
-  // 2: A = (B T1) ./ D   left outT[m][i] = B[i][m]
-  fdc_gemm(acc, outT, n1, j, active, rch, [&](int m) { return __ldg(it.T1 + (size_t)m * n1 + jj); });
-  if (active) {
+  // 2: A = (B T1) ./ D    left outT[m][i] = B[i][m]
+  fdc_gemm<RB>(acc, outT, n1, c.j, rch, [&](int m) { return __ldg(c.it.T1 + (size_t)m * n1 + jj); });
+  if (c.active) {
 #pragma unroll
-    for (int i = 0; i < FDC_RB; ++i)
-      if (i < nr) {
-        const size_t o = (size_t)(r0 + i) * n1 + j;
-        __stcg(it.scratch + o, __ddiv_rn(acc[i], __ldg(it.D + o)));
+    for (int i = 0; i < RB; ++i)
+      if (i < c.nr) {
+        const size_t o = (size_t)(c.r0 + i) * n1 + c.j;
+        c.it.scratch[o] = __ddiv_rn(acc[i], __ldg(c.it.D + o));
       }
   }
-  cluster.sync();  // every row of A written (release/acquire at cluster scope)
-  // 3: B' = T0 A        lop[m][i] = T0[r0 + i][m]
-  fill(true);
-  int gi[FDC_RB];  // epilogue targets, fetched two products ahead (idx -> u chain off the critical path)
+}
+
+template <int RB>
+__global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, double* u, double alpha,
+                                                         int accumulate) {
+  extern __shared__ __align__(16) double fdc_smem[];
+  double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
+  double (*outT)[RB] = lop + FDC_NMAX;
+  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(fdc_smem + 2 * FDC_NMAX * RB);
+  const FdCtx c = fd_locate(bt);
+  const int n1 = c.n1, jj = c.jj;
+  double acc[RB];
+  // 3: B' = T0 A
+  fd_fill<RB>(lop, c, true);
+  int gi[RB];  // epilogue targets, fetched two products ahead
 #pragma unroll
-  for (int i = 0; i < FDC_RB; ++i) gi[i] = __ldg(it.idx + (size_t)(r0 + min(i, max(nr - 1, 0))) * n1 + jj);
+  for (int i = 0; i < RB; ++i) gi[i] = __ldg(c.it.idx + (size_t)(c.r0 + min(i, max(c.nr - 1, 0))) * n1 + jj);
   __syncthreads();
-  fdc_gemm(acc, lop, n0, j, active, rch, [&](int m) { return __ldcg(it.scratch + (size_t)m * n1 + jj); });
-  __syncthreads();
+  fdc_gemm<RB>(acc, lop, c.n0, c.j, rch, [&](int m) { return c.it.scratch[(size_t)m * n1 + jj]; });
 #pragma unroll
-  for (int i = 0; i < FDC_RB; ++i) outT[j][i] = acc[i];
+  for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
   __syncthreads();
-  // 4: X = B' T1^T      right T1[j][m]
-  fdc_gemm(acc, outT, n1, j, active, rch, [&](int m) { return __ldg(it.T1 + (size_t)jj * n1 + m); });
-  if (active) {
+  // 4: X = B' T1^T       right T1[j][m]
+  fdc_gemm<RB>(acc, outT, n1, c.j, rch, [&](int m) { return __ldg(c.it.T1 + (size_t)jj * n1 + m); });
+  if (c.active) {
 #pragma unroll
-    for (int i = 0; i < FDC_RB; ++i)
-      if (i < nr) {
+    for (int i = 0; i < RB; ++i)
+      if (i < c.nr) {
         const double v = __dmul_rn(alpha, acc[i]);
         u[gi[i]] = accumulate ? __dadd_rn(u[gi[i]], v) : v;
       }
   }
 }
 
+template <int RB>
+void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(fd_front_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>());
+    cudaFuncSetAttribute(fd_back_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>());
+    attr = true;
+  }
+  const int grid = bt.cta0[bt.nitems];
+  fd_front_kernel<RB><<<grid, FDC_NT, fd_smem<RB>(), s>>>(bt, r);
+  fd_back_kernel<RB><<<grid, FDC_NT, fd_smem<RB>(), s>>>(bt, u, alpha, accumulate);
+}
+
 }  // namespace
 
-int fd_cluster_size(int n0max) { return (n0max + FDC_RB - 1) / FDC_RB; }
+int fd_rows_per_cta(int total_rows) {
+  // about two CTAs per SM for the level's interiors together
+  const int want = (total_rows + 295) / 296;
+  return want <= 2 ? 2 : (want <= 4 ? 4 : 8);
+}
+
+void launch_fd_batch(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate) {
+  if (bt.nitems <= 0) return;
+  switch (bt.rb) {
+    case 2: launch_rb<2>(s, bt, r, u, alpha, accumulate); break;
+    case 4: launch_rb<4>(s, bt, r, u, alpha, accumulate); break;
+    default: launch_rb<8>(s, bt, r, u, alpha, accumulate); break;
+  }
+}
 
 void set_carveout_panel(int pct);  // panel.cu
 
 void set_carveout_panel_fd(int pct) {
-  cudaFuncSetAttribute(fd_cluster_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
+  for (const void* f : {(const void*)fd_front_kernel<2>, (const void*)fd_back_kernel<2>, (const void*)fd_front_kernel<4>,
+                        (const void*)fd_back_kernel<4>, (const void*)fd_front_kernel<8>, (const void*)fd_back_kernel<8>})
+    cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaGetLastError();
   set_carveout_panel(pct);
-}
-
-void launch_fd_cluster(cudaStream_t s, const FdCluster* d_items, int nitems, int G, const double* r, double* u,
-                       double alpha, int accumulate) {
-  if (nitems <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fd_cluster_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    cudaFuncSetAttribute(fd_cluster_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FDC_SMEM);
-    attr = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nitems * G, 1, 1);
-  cfg.blockDim = dim3(FDC_NT, 1, 1);
-  cfg.dynamicSmemBytes = FDC_SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute attrs[1];
-  attrs[0].id = cudaLaunchAttributeClusterDimension;
-  attrs[0].val.clusterDim.x = G;
-  attrs[0].val.clusterDim.y = 1;
-  attrs[0].val.clusterDim.z = 1;
-  cfg.attrs = attrs;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, fd_cluster_kernel, d_items, r, u, alpha, accumulate);
 }
 
 }  // namespace igb

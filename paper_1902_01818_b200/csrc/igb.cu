@@ -72,9 +72,8 @@ struct InteriorStage {
 };
 
 struct FdPlan {
-  FdCluster* d_clu = nullptr;   // fused 2-D interiors, one cluster each
-  int nclu = 0, clu_G = 1;
-  double clu_bytes = 0;
+  std::vector<FdBatch> batches;  // fused 2-D interiors (fd.cu)
+  std::vector<double> batch_bytes;
   int nsteps = 0;
   GemmDesc* d_desc[6] = {nullptr};
   int ndesc[6] = {0};
@@ -378,9 +377,9 @@ struct igb_ctx {
   void scms(int l, const double* res, double* u, bool u_zero) {
     Level& V = lev[l];
     const FdPlan& F = V.fd;
-    if (F.nclu) {
-      launch(K_FD, F.clu_bytes, [&] {
-        launch_fd_cluster(stream, F.d_clu, F.nclu, F.clu_G, res, u, V.tau, u_zero ? 0 : 1);
+    for (size_t b = 0; b < F.batches.size(); ++b) {
+      launch(K_FD, F.batch_bytes[b], [&] {
+        launch_fd_batch(stream, F.batches[b], res, u, V.tau, u_zero ? 0 : 1);
       });
     }
     for (int s = 0; s < F.nsteps; ++s) {
@@ -648,15 +647,10 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
   std::vector<FdCluster> clu;
   std::vector<InteriorStage> big;
   const bool fuse = !(std::getenv("IGB_FD_FUSE") && std::string(std::getenv("IGB_FD_FUSE")) == "0");
-  int n0max = 0;
   for (auto& it : V.interiors) {
     if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
     if (fuse && dim == 2 && it.n[0] <= FDC_NMAX && it.n[1] <= FDC_NMAX) {
-      FdCluster f{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]};
-      clu.push_back(f);
-      n0max = std::max(n0max, it.n[0]);
-      // T0 and T1 read twice, R gathered, D, A written + read, X scattered
-      V.fd.clu_bytes += 16.0 * (it.n[0] * it.n[0] + it.n[1] * it.n[1]) + (12.0 + 8 + 16 + 12) * it.n[0] * it.n[1];
+      clu.push_back(FdCluster{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]});
     } else {
       big.push_back(it);
     }
@@ -669,9 +663,24 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
       f.scratch = scratch;
       scratch += (size_t)f.n0 * f.n1;
     }
-    V.fd.d_clu = ctx->upload(clu.data(), clu.size());
-    V.fd.nclu = (int)clu.size();
-    V.fd.clu_G = fd_cluster_size(n0max);
+    for (size_t b0 = 0; b0 < clu.size(); b0 += FD_BATCH_MAX) {
+      FdBatch bt{};
+      bt.nitems = (int)std::min<size_t>(FD_BATCH_MAX, clu.size() - b0);
+      int rows = 0;
+      double bytes = 0;
+      for (int i = 0; i < bt.nitems; ++i) {
+        bt.items[i] = clu[b0 + i];
+        rows += bt.items[i].n0;
+        const double n0 = bt.items[i].n0, n1 = bt.items[i].n1;
+        // T0 and T1 read twice, R gathered, D, A written + read, X scattered
+        bytes += 16.0 * (n0 * n0 + n1 * n1) + (12.0 + 8 + 16 + 12) * n0 * n1;
+      }
+      bt.rb = fd_rows_per_cta(rows);
+      bt.cta0[0] = 0;
+      for (int i = 0; i < bt.nitems; ++i) bt.cta0[i + 1] = bt.cta0[i] + (bt.items[i].n0 + bt.rb - 1) / bt.rb;
+      V.fd.batches.push_back(bt);
+      V.fd.batch_bytes.push_back(bytes);
+    }
   }
   V.interiors = big;
   if (big.empty()) return;

@@ -150,11 +150,12 @@ constexpr int FD_SMALL_NMAX = 80;
 void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
                      double alpha, int accumulate);
 
-// ---- fused 2-D fast diagonalisation, one thread-block cluster per interior (fd.cu) --
-// n0, n1 <= FDC_NMAX; G = fd_cluster_size(max n0) CTAs of FDC_NT threads per interior;
-// scratch: n0 * n1 doubles per interior (the middle intermediate, exchanged through L2).
+// ---- fused 2-D fast diagonalisation (fd.cu): two launches per application, RB rows of
+// one interior per CTA, all interiors of a level (up to FD_BATCH_MAX per batch) in one grid.
+// n0, n1 <= FDC_NMAX; scratch: n0 * n1 doubles per interior (the middle intermediate).
 constexpr int FDC_NMAX = 160;
 constexpr int FDC_NT = 160;
+constexpr int FD_BATCH_MAX = 16;
 struct FdCluster {
   const double* T0;
   const double* T1;
@@ -163,9 +164,14 @@ struct FdCluster {
   double* scratch;
   int n0, n1;
 };
-int fd_cluster_size(int n0max);
-void launch_fd_cluster(cudaStream_t s, const FdCluster* d_items, int nitems, int G, const double* r, double* u,
-                       double alpha, int accumulate);
+struct FdBatch {
+  FdCluster items[FD_BATCH_MAX];
+  int cta0[FD_BATCH_MAX + 1];  // first CTA of each item; cta0[nitems] = grid size
+  int nitems;
+  int rb;                      // rows per CTA: 2, 4 or 8
+};
+int fd_rows_per_cta(int total_rows);
+void launch_fd_batch(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate);
 
 // ---- interface-piece dense solves (precomputed inverses) ---------------------
 struct PieceRowBlock {

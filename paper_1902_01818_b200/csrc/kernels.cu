@@ -703,6 +703,16 @@ __global__ void __launch_bounds__(256) cg_direction_kernel(int n, double* __rest
     d[i] = __dadd_rn(z[i], __dmul_rn(beta, d[i]));
 }
 
+// Conditions of the device-resident PCG loop (igb.cu: build_pcg_graph).  start: run the loop
+// at all (||b|| != 0, max_iters > 0); else: continue after this iteration's update.
+__global__ void cg_cond_kernel(cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
+                               const CgScalars* sc, int max_iters, int start) {
+  if (threadIdx.x != 0) return;
+  const unsigned cont = start ? (sc->normb != 0.0 && max_iters > 0) : (!sc->done && sc->it < max_iters);
+  cudaGraphSetConditional(loop, cont);
+  if (!start) cudaGraphSetConditional(more, cont);
+}
+
 __global__ void copy_kernel(int n, double* __restrict__ dst, const double* __restrict__ src) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = src[i];
@@ -878,6 +888,11 @@ void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double*
                       const double* q, double* partials, unsigned* counter, CgScalars* sc,
                       double* hist) {
   cg_update_kernel<<<reduction_grid(n), 256, 0, s>>>(n, x, r, d, q, partials, counter, sc, hist);
+}
+
+void launch_cg_cond(cudaStream_t s, cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
+                    const CgScalars* sc, int max_iters, int start) {
+  cg_cond_kernel<<<1, 32, 0, s>>>(loop, more, sc, max_iters, start);
 }
 
 void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc) {

@@ -207,6 +207,9 @@ void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double*
                       double* hist);
 // d = z + beta d
 void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc);
+// sets the WHILE (loop) and IF (more) conditions of the device-resident PCG graph
+void launch_cg_cond(cudaStream_t s, cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
+                    const CgScalars* sc, int max_iters, int start);
 void launch_copy(cudaStream_t s, int n, double* dst, const double* src);
 void launch_fill(cudaStream_t s, int n, double* dst, double v);
 

@@ -143,9 +143,31 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_front_kernel(const __grid_consta
   }
 }
 
+// interface pieces (linsolve.py:33-53 on the pieces of smoothers.py:316-319): u[idx] (+)=
+// alpha inv r[idx], warp per row -- the same work as piece_gemv_kernel, in the back launch
+__device__ void fd_piece_rows(const PieceRowBlock& b, const double* r, double* u, double alpha, int accumulate) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp >= b.nrows) return;
+  const int i = b.row0 + warp;
+  const double* row = b.inv + (long long)i * b.m;
+  double s = 0.0;
+  for (int j = lane; j < b.m; j += 32) s = fma(__ldg(&row[j]), __ldg(&r[__ldg(&b.idx[j])]), s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    const int gi = __ldg(&b.idx[i]);
+    const double v = __dmul_rn(alpha, s);
+    u[gi] = accumulate ? __dadd_rn(u[gi], v) : v;
+  }
+}
+
 template <int RB>
-__global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, double* u, double alpha,
-                                                         int accumulate) {
+__global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, const double* r,
+                                                         double* u, double alpha, int accumulate) {
+  if ((int)blockIdx.x >= bt.cta0[bt.nitems]) {
+    fd_piece_rows(bt.pieces[blockIdx.x - bt.cta0[bt.nitems]], r, u, alpha, accumulate);
+    return;
+  }
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
   double (*outT)[RB] = lop + FDC_NMAX;
@@ -185,7 +207,7 @@ void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, do
   }
   const int grid = bt.cta0[bt.nitems];
   fd_front_kernel<RB><<<grid, FDC_NT, fd_smem<RB>(), s>>>(bt, r);
-  fd_back_kernel<RB><<<grid, FDC_NT, fd_smem<RB>(), s>>>(bt, u, alpha, accumulate);
+  fd_back_kernel<RB><<<grid + bt.npieces, FDC_NT, fd_smem<RB>(), s>>>(bt, r, u, alpha, accumulate);
 }
 
 }  // namespace

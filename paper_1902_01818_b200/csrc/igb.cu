@@ -113,6 +113,8 @@ struct Level {
   bool has_P = false;
   DevCsr P, PT;
   bool has_gs = false;
+  bool has_U = false;
+  DevCsr U;  // strict upper triangle of A: residual after a forward sweep from zero is -U c
   Sched fwd, bwd;
   long long tri_nnz_lower = 0, tri_nnz_upper = 0;
   bool has_scms = false;
@@ -121,6 +123,7 @@ struct Level {
   std::vector<PieceRowBlock> h_blocks;
   PieceRowBlock* d_blocks = nullptr;
   double piece_bytes = 0;
+  bool pieces_fused = false;  // done by the FD back kernel's extra CTAs
   long long piece_rows = 0;
   FdPlan fd;
   size_t fd_scratch = 0;
@@ -396,7 +399,7 @@ struct igb_ctx {
         launch_fd_gemm(stream, F.d_desc[s], F.ndesc[s], F.tiles[s], res, u, V.tau, u_zero ? 0 : 1);
       });
     }
-    if (!V.h_blocks.empty()) {
+    if (!V.h_blocks.empty() && !V.pieces_fused) {
       launch(K_PIECES, V.piece_bytes, [&] {
         launch_piece_gemv(stream, V.d_blocks, (int)V.h_blocks.size(), res, u, V.tau, u_zero ? 0 : 1);
       });
@@ -455,8 +458,18 @@ struct igb_ctx {
     } else if (smoother == IGB_SMOOTHER_SCMS) {
       for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
     } else {
+      const bool from_zero = uz;
       smooth_step(l, 'G', f, u, uz);
-      for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
+      for (int i = 0; i < st; ++i) {
+        Level& V = lev[l];
+        if (i == 0 && from_zero && V.has_U) {
+          // u = c with tril(A) c = f, so f - A u = -triu(A, 1) c: half the matrix traffic
+          spmv(V.U, u, nullptr, V.r, -1, K_SPMV);
+          scms(l, V.r, u, false);
+        } else {
+          smooth_step(l, 'S', f, u, uz);
+        }
+      }
     }
   }
   void post_smooth(int l, const double* f, double* u, bool& uz) {
@@ -907,37 +920,35 @@ int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long
 // CTAs (B = 512) if the device can host it, else 8 (B = 256).
 bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp, int nlev,
                        bool force) {
-  static int G = -1;
-  if (G < 0) {
-    G = 0;
-    const char* genv = std::getenv("IGB_PANEL_G");
-    const int want = genv ? std::atoi(genv) : 16;
-    for (int g : {16, 8})
-      if (g <= want && panel_prepare(g, g + 1)) {
-        G = g;
-        break;
-      }
+  // shapes: B = 512 (16 warps, 8K ring) first; B = 256 (8 warps, 16K ring, more entry slots
+  // per row) when the rows carry more entries than the first shape's kernel variants hold
+  static int shapes_ok = -1;  // bit 0: KBC 17, bit 1: KBC 9
+  static int max_clu[2] = {1, 1};
+  const int G = 16;
+  if (shapes_ok < 0) {
+    shapes_ok = (panel_prepare(G, 17) ? 1 : 0) | (panel_prepare(G, 9) ? 2 : 0);
+    for (int sh = 0; sh < 2; ++sh) {
+      PanelArgs probe{};
+      probe.KBC = sh ? 9 : 17;
+      probe.B = sh ? 256 : 512;
+      probe.R = sh ? 16384 : 8192;
+      max_clu[sh] = panel_max_clusters(G, probe.KBC, panel_smem_bytes(probe));
+      if (const char* ce = std::getenv("IGB_PANEL_CLUSTERS"))
+        max_clu[sh] = std::max(1, std::min(max_clu[sh], std::atoi(ce)));
+      max_clu[sh] = std::min(max_clu[sh], 8);
+    }
   }
-  if (!G) return false;
-  const int B = 32 * G;
-  const int npan = (V.n + B - 1) / B;
-  if (!force && 2 * npan > nlev) return false;
   PanelPlanHost plan;
-  const int R = 8192;
-  // concurrent clusters (panel ranges): all of them must be co-resident
-  static int max_clu = -1;
-  if (max_clu < 0) {
-    PanelArgs probe{};
-    probe.R = R;
-    probe.B = B;
-    probe.KBC = G + 1;
-    max_clu = panel_max_clusters(G, G + 1, panel_smem_bytes(probe));
-    if (const char* ce = std::getenv("IGB_PANEL_CLUSTERS")) max_clu = std::max(1, std::min(max_clu, std::atoi(ce)));
-    max_clu = std::min(max_clu, 8);
+  bool built = false;
+  for (int sh = 0; sh < 2 && !built; ++sh) {
+    if (!(shapes_ok >> sh & 1)) continue;
+    const int W = sh ? 8 : 16, R = sh ? 16384 : 8192, B = 2 * G * W;
+    const int npan = (V.n + B - 1) / B;
+    if (!force && 2 * npan > nlev) continue;
+    built = build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, W, R,
+                             max_clu[sh], plan);
   }
-  if (!build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, R, max_clu,
-                        plan))
-    return false;
+  if (!built) return false;
   PanelDev& P = V.panel[dir];
   PanelArgs& a = P.args;
   a = PanelArgs{};
@@ -997,6 +1008,19 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     Level& V = ctx->level(level);
     if (!V.n) throw StateError("set the level matrix before igb_set_gs");
     std::vector<int> dp = diag_positions(V.n, V.h_ptr.data(), V.h_col.data(), nullptr, "A");
+    {
+      std::vector<int> up(V.n + 1, 0), ui;
+      std::vector<double> uv;
+      for (int i = 0; i < V.n; ++i) {
+        for (int j = dp[i] + 1; j < V.h_ptr[i + 1]; ++j) {
+          ui.push_back(V.h_col[j]);
+          uv.push_back(V.h_val[j]);
+        }
+        up[i + 1] = (int)ui.size();
+      }
+      V.U = upload_csr(ctx, V.n, V.n, (long long)ui.size(), up.data(), ui.data(), uv.data());
+      V.has_U = !(std::getenv("IGB_GS_RESIDUAL") && std::string(std::getenv("IGB_GS_RESIDUAL")) == "full");
+    }
     V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);
     V.bwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, true);
     const char* eng = std::getenv("IGB_GS_ENGINE");
@@ -1275,6 +1299,18 @@ int igb_finalize(igb_ctx* ctx) {
       if (V.has_scms) {
         build_fd_plan(ctx, V);
         if (!V.h_blocks.empty()) V.d_blocks = ctx->upload(V.h_blocks.data(), V.h_blocks.size());
+        if (!V.h_blocks.empty() && !V.fd.batches.empty()) {
+          // piece rows in blocks of 5 (the FD kernels' warps), appended to the last FD batch
+          std::vector<PieceRowBlock> five;
+          for (const auto& b : V.h_blocks)
+            for (int r0 = b.row0; r0 < b.row0 + b.nrows; r0 += 5)
+              five.push_back(PieceRowBlock{b.inv, b.idx, b.m, r0, std::min(5, b.row0 + b.nrows - r0)});
+          FdBatch& bt = V.fd.batches.back();
+          bt.pieces = ctx->upload(five.data(), five.size());
+          bt.npieces = (int)five.size();
+          V.fd.batch_bytes.back() += V.piece_bytes;
+          V.pieces_fused = true;
+        }
         // the pieces must partition 0..n-1 together with the interiors
       }
       V.h_col.clear();

@@ -105,7 +105,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict_
   for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if (row < n && lane == 0) {
     if (sign == 0) y[row] = s;
-    else if (sign < 0) y[row] = __dsub_rn(z[row], s);
+    else if (sign < 0) y[row] = z ? __dsub_rn(z[row], s) : -s;
     else y[row] = __dadd_rn(z[row], s);
   }
 }

@@ -17,7 +17,7 @@ namespace igb {
 void carveout_prepare();
 void set_carveout_panel_fd(int pct);   // panel.cu / fd.cu kernels
 
-// ---- CSR SpMV: y = z + sign * A x  (sign 0: y = A x) -----------------------
+// ---- CSR SpMV: y = z + sign * A x  (sign 0: y = A x; sign < 0 and z null: y = -A x) ------
 void launch_spmv(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,
                  const double* x, const double* z, double* y, int sign, int group);
 
@@ -72,7 +72,7 @@ void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in
 void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* xp, double* u, int accumulate);
 
 // ---- row-panel triangular sweep (Gauss-Seidel in natural order), one cluster ----
-// See panel_plan.h: G CTAs x PANEL_W warps, panels of B = 32 G rows, inverse blocks
+// See panel_plan.h: G CTAs x W warps (16 or 8), panels of B = 2 G W rows, inverse blocks
 // streamed by TMA, recent solution values in a DSMEM-broadcast ring of R slots.
 constexpr int PANEL_W = 16;
 constexpr int PANEL_STAGES = 2;   // TMA stages of the inverse slices (power of two)
@@ -150,6 +150,15 @@ constexpr int FD_SMALL_NMAX = 80;
 void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
                      double alpha, int accumulate);
 
+// ---- interface-piece dense solves (precomputed inverses) ---------------------
+struct PieceRowBlock {
+  const double* inv;   // m x m
+  const int* idx;      // m
+  int m;
+  int row0;            // first row handled by this block
+  int nrows;           // rows in this block (<= warps per block)
+};
+
 // ---- fused 2-D fast diagonalisation (fd.cu): two launches per application, RB rows of
 // one interior per CTA, all interiors of a level (up to FD_BATCH_MAX per batch) in one grid.
 // n0, n1 <= FDC_NMAX; scratch: n0 * n1 doubles per interior (the middle intermediate).
@@ -169,18 +178,12 @@ struct FdBatch {
   int cta0[FD_BATCH_MAX + 1];  // first CTA of each item; cta0[nitems] = grid size
   int nitems;
   int rb;                      // rows per CTA: 2, 4 or 8
+  const PieceRowBlock* pieces; // interface-piece rows (<= 5 per block) done by extra CTAs of
+  int npieces;                 // the back kernel (disjoint u entries), or none
 };
 int fd_rows_per_cta(int total_rows);
 void launch_fd_batch(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate);
 
-// ---- interface-piece dense solves (precomputed inverses) ---------------------
-struct PieceRowBlock {
-  const double* inv;   // m x m
-  const int* idx;      // m
-  int m;
-  int row0;            // first row handled by this block
-  int nrows;           // rows in this block (<= warps per block)
-};
 void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
                        const double* r, double* u, double tau, int accumulate);
 

@@ -168,11 +168,16 @@ struct PanelSet {
 // for a later one.
 
 
+// warps per CTA by inverse-chunk count: B = 512 (16 warps) or B = 256 (8 warps, more
+// registers per thread for the entry-heavy 3-D rows)
+template <int KBC>
+__host__ __device__ constexpr int panel_warps() { return KBC == 17 ? 16 : 8; }
+
 template <int KBC, int KA, int KF>
-__global__ void __launch_bounds__(PANEL_W * 32, 1) panel_sweep_kernel(PanelArgs a) {
+__global__ void __launch_bounds__(panel_warps<KBC>() * 32, 1) panel_sweep_kernel(PanelArgs a) {
   using Set = PanelSet<KA, KF>;
   extern __shared__ __align__(128) double psm[];
-  constexpr int W = PANEL_W;
+  constexpr int W = panel_warps<KBC>();
   constexpr int S = PANEL_STAGES;
   const int B = a.B, R = a.R, n = a.n;
   const cg::cluster_group cluster = cg::this_cluster();
@@ -418,7 +423,7 @@ void launch_one(cudaStream_t st, const PanelArgs& a) {
   auto kern = panel_sweep_kernel<KBC, KA, KF>;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(a.G * a.nclu, 1, 1);
-  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.blockDim = dim3(panel_warps<KBC>() * 32, 1, 1);
   cfg.dynamicSmemBytes = panel_smem_bytes(a);
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -431,47 +436,49 @@ void launch_one(cudaStream_t st, const PanelArgs& a) {
   cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-template <int KBC, int KA>
-void dispatch_kf(cudaStream_t st, const PanelArgs& a) {
+// variants: B = 512: KA in {2,4,8,12}, KF in {0,1,4};  B = 256: KA in {4,8,12}, KF in {0,4,8}
+template <int KA>
+void dispatch_kf17(cudaStream_t st, const PanelArgs& a) {
   switch (a.KF) {
-    case 0: launch_one<KBC, KA, 0>(st, a); break;
-    case 1: launch_one<KBC, KA, 1>(st, a); break;
-    default: launch_one<KBC, KA, 4>(st, a); break;
+    case 0: launch_one<17, KA, 0>(st, a); break;
+    case 1: launch_one<17, KA, 1>(st, a); break;
+    default: launch_one<17, KA, 4>(st, a); break;
   }
 }
-
-template <int KBC>
-void dispatch_ka(cudaStream_t st, const PanelArgs& a) {
-  switch (a.KA) {
-    case 2: dispatch_kf<KBC, 2>(st, a); break;
-    case 4: dispatch_kf<KBC, 4>(st, a); break;
-    case 8: dispatch_kf<KBC, 8>(st, a); break;
-    default: dispatch_kf<KBC, 12>(st, a); break;
+template <int KA>
+void dispatch_kf9(cudaStream_t st, const PanelArgs& a) {
+  switch (a.KF) {
+    case 0: launch_one<9, KA, 0>(st, a); break;
+    case 4: launch_one<9, KA, 4>(st, a); break;
+    default: launch_one<9, KA, 8>(st, a); break;
   }
 }
 
 template <class F>
 void for_all_variants(int KBC, F&& f) {
-  auto per_ka = [&](auto kbc, auto ka) {
-    constexpr int C = decltype(kbc)::value, K = decltype(ka)::value;
-    f(panel_sweep_kernel<C, K, 0>);
-    f(panel_sweep_kernel<C, K, 1>);
-    f(panel_sweep_kernel<C, K, 4>);
+  auto per_ka = [&](auto ka) {
+    constexpr int K = decltype(ka)::value;
+    if (KBC == 17) {
+      f(panel_sweep_kernel<17, K, 0>);
+      f(panel_sweep_kernel<17, K, 1>);
+      f(panel_sweep_kernel<17, K, 4>);
+    } else if (K >= 4) {
+      f(panel_sweep_kernel<9, (K >= 4 ? K : 4), 0>);
+      f(panel_sweep_kernel<9, (K >= 4 ? K : 4), 4>);
+      f(panel_sweep_kernel<9, (K >= 4 ? K : 4), 8>);
+    }
   };
-  auto per_kbc = [&](auto kbc) {
-    per_ka(kbc, std::integral_constant<int, 2>{});
-    per_ka(kbc, std::integral_constant<int, 4>{});
-    per_ka(kbc, std::integral_constant<int, 8>{});
-    per_ka(kbc, std::integral_constant<int, 12>{});
-  };
-  if (KBC == 17) per_kbc(std::integral_constant<int, 17>{});
-  else per_kbc(std::integral_constant<int, 9>{});
+  per_ka(std::integral_constant<int, 2>{});
+  per_ka(std::integral_constant<int, 4>{});
+  per_ka(std::integral_constant<int, 8>{});
+  per_ka(std::integral_constant<int, 12>{});
 }
 
 }  // namespace
 
 size_t panel_smem_bytes(const PanelArgs& a) {
-  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)PANEL_STAGES * PANEL_W * a.KBC * 32) + 8 * ((size_t)PANEL_STAGES + 3);
+  const size_t W = a.KBC == 17 ? 16 : 8;
+  return 8 * ((size_t)a.R + 2 * (size_t)a.B + (size_t)PANEL_STAGES * W * a.KBC * 32) + 8 * ((size_t)PANEL_STAGES + 3);
 }
 
 bool panel_prepare(int G, int KBC) {
@@ -490,7 +497,7 @@ bool panel_prepare(int G, int KBC) {
   // can a cluster of G CTAs with (nearly) all shared memory be resident?
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G, 1, 1);
-  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.blockDim = dim3((KBC == 17 ? 16 : 8) * 32, 1, 1);
   cfg.dynamicSmemBytes = 220 * 1024;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -501,7 +508,7 @@ bool panel_prepare(int G, int KBC) {
   cfg.numAttrs = 1;
   int nclusters = 0;
   cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 0>, &cfg)
-                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 0>, &cfg);
+                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 4, 0>, &cfg);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return false;
@@ -518,7 +525,7 @@ void set_carveout_panel(int pct) {
 int panel_max_clusters(int G, int KBC, size_t smem) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(G * 8, 1, 1);
-  cfg.blockDim = dim3(PANEL_W * 32, 1, 1);
+  cfg.blockDim = dim3((KBC == 17 ? 16 : 8) * 32, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -529,7 +536,7 @@ int panel_max_clusters(int G, int KBC, size_t smem) {
   cfg.numAttrs = 1;
   int nclusters = 0;
   cudaError_t e = KBC == 17 ? cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<17, 2, 4>, &cfg)
-                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 2, 4>, &cfg);
+                            : cudaOccupancyMaxActiveClusters(&nclusters, panel_sweep_kernel<9, 4, 8>, &cfg);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return 1;
@@ -538,8 +545,20 @@ int panel_max_clusters(int G, int KBC, size_t smem) {
 }
 
 void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {
-  if (a.KBC == 17) dispatch_ka<17>(st, a);
-  else dispatch_ka<9>(st, a);
+  if (a.KBC == 17) {
+    switch (a.KA) {
+      case 2: dispatch_kf17<2>(st, a); break;
+      case 4: dispatch_kf17<4>(st, a); break;
+      case 8: dispatch_kf17<8>(st, a); break;
+      default: dispatch_kf17<12>(st, a); break;
+    }
+  } else {
+    switch (a.KA) {
+      case 4: dispatch_kf9<4>(st, a); break;
+      case 8: dispatch_kf9<8>(st, a); break;
+      default: dispatch_kf9<12>(st, a); break;
+    }
+  }
 }
 
 }  // namespace igb

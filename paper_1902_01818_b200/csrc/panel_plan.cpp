@@ -58,8 +58,8 @@ double simulate_ranges(int n, int B, const std::vector<int>& rs, MaxRef maxref) 
 }  // namespace
 
 bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos,
-                      bool upper, int G, int R, int max_clusters, PanelPlanHost& out) {
-  const int W = 16;
+                      bool upper, int G, int W, int R, int max_clusters, PanelPlanHost& out) {
+  if (W != 16 && W != 8) return false;
   const int B = 2 * G * W;
   if (n <= 0 || (R & (R - 1)) || R < B) return false;
   out = PanelPlanHost{};
@@ -154,11 +154,12 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
     out.near_entries += nn;
     out.far_entries += nf;
   }
-  out.KA = round_up_variant((max_near + 15) / 16, {2, 4, 8, 12});
-  out.KF = round_up_variant((max_far + 15) / 16, {0, 1, 4});
+  out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12})
+                   : round_up_variant((max_near + 15) / 16, {4, 8, 12});
+  out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4}) : round_up_variant((max_far + 15) / 16, {0, 4, 8});
   if (out.KA < 0 || out.KF < 0) {
     // cross-range references overflowed the kernel variants: one range (if that fits)
-    if (out.nclu > 1) return build_panel_plan(n, ptr, col, val, dpos, upper, G, R, 1, out);
+    if (out.nclu > 1) return build_panel_plan(n, ptr, col, val, dpos, upper, G, W, R, 1, out);
     return false;
   }
   const int KA = out.KA, KF = out.KF, KBC = out.KBC;

@@ -117,6 +117,7 @@ __device__ __forceinline__ void fd_fill(double (*lop)[RB], const FdCtx& c, bool 
 
 template <int RB>
 __global__ void __launch_bounds__(FDC_NT, 2) fd_front_kernel(const __grid_constant__ FdBatch bt, const double* r) {
+  pdl_begin();
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
   double (*outT)[RB] = lop + FDC_NMAX;
@@ -164,6 +165,7 @@ __device__ void fd_piece_rows(const PieceRowBlock& b, const double* r, double* u
 template <int RB>
 __global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, const double* r,
                                                          double* u, double alpha, int accumulate) {
+  pdl_begin();
   if ((int)blockIdx.x >= bt.cta0[bt.nitems]) {
     fd_piece_rows(bt.pieces[blockIdx.x - bt.cta0[bt.nitems]], r, u, alpha, accumulate);
     return;
@@ -206,8 +208,8 @@ void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, do
     attr = true;
   }
   const int grid = bt.cta0[bt.nitems];
-  fd_front_kernel<RB><<<grid, FDC_NT, fd_smem<RB>(), s>>>(bt, r);
-  fd_back_kernel<RB><<<grid + bt.npieces, FDC_NT, fd_smem<RB>(), s>>>(bt, r, u, alpha, accumulate);
+  launch_k(fd_front_kernel<RB>, dim3(grid), dim3(FDC_NT), fd_smem<RB>(), s, bt, r);
+  launch_k(fd_back_kernel<RB>, dim3(grid + bt.npieces), dim3(FDC_NT), fd_smem<RB>(), s, bt, r, u, alpha, accumulate);
 }
 
 }  // namespace

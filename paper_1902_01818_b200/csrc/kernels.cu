@@ -93,6 +93,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict_
                                                    const double* __restrict__ val,
                                                    const double* __restrict__ x,
                                                    const double* z, double* y, int sign) {
+  pdl_begin();
   const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const int row = (int)(gt / G);
   const int lane = (int)(gt % G);
@@ -118,6 +119,7 @@ __global__ void __launch_bounds__(256) spmv_dot_kernel(int n, const int* __restr
                                                        double* __restrict__ q, double* partials,
                                                        unsigned* counter, CgScalars* sc,
                                                        double* hist) {
+  pdl_begin();
   __shared__ double red[32];
   if (sc->done) return;
   const int rows_per_block = blockDim.x / G;
@@ -170,6 +172,7 @@ __device__ void trsv_phase(const TrsvPhase& P) {
 __global__ void __launch_bounds__(1024) sptrsv_kernel(TrsvPhase a, TrsvPhase b, int has_b,
                                                       int n_out, const int* __restrict__ out_idx,
                                                       double* out) {
+  pdl_begin();
   trsv_phase(a);
   if (has_b) trsv_phase(b);
   if (out) {
@@ -247,6 +250,7 @@ struct LvlSet {
 // each CTA issues a TMA bulk L2 prefetch of block t+PF.
 template <bool OLD, bool CLUSTER>
 __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
+  pdl_begin();
   extern __shared__ __align__(16) double lsm[];
   double* ring = lsm;
   const int4* meta = reinterpret_cast<const int4*>(a.meta);  // read-only, L1-cached, used 3 steps ahead
@@ -382,12 +386,14 @@ __global__ void __launch_bounds__(LEVEL_NT) level_sweep_kernel(LevelArgs a) {
 
 __global__ void perm_gather_kernel(int n, const int* __restrict__ rows, const double* __restrict__ in,
                                    double* __restrict__ out) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     out[i] = in[__ldg(&rows[i])];
 }
 
 __global__ void perm_scatter_kernel(int n, const int* __restrict__ rows, const double* __restrict__ xp,
                                     double* __restrict__ u, int accumulate) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int r = __ldg(&rows[i]);
     u[r] = accumulate ? __dadd_rn(u[r], xp[i]) : xp[i];
@@ -402,6 +408,7 @@ __global__ void perm_scatter_kernel(int n, const int* __restrict__ rows, const d
 template <bool RESIDENT>
 __global__ void __launch_bounds__(1024) coarse_csc_kernel(CoarseCsc c, const double* __restrict__ rhs,
                                                           double* __restrict__ out) {
+  pdl_begin();
   extern __shared__ double y[];
   const int n = c.n;
   const int NT = blockDim.x, tid = threadIdx.x;
@@ -459,6 +466,7 @@ constexpr int FD_BM = 64, FD_BN = 64, FD_BK = 16;
 __global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict__ descs,
                                                       int ndesc, const double* __restrict__ gsrc,
                                                       double* sdst, double alpha, int accumulate) {
+  pdl_begin();
   __shared__ double As[FD_BK][FD_BM + 1];
   __shared__ double Bs[FD_BK][FD_BN + 1];
   const int t = blockIdx.x;
@@ -581,6 +589,7 @@ __device__ __forceinline__ void fds_block(double (&acc)[FDS_B][FDS_B], const dou
 __global__ void __launch_bounds__(256) fd_small_kernel(const FdSmall* __restrict__ items,
                                                        const double* __restrict__ r, double* u,
                                                        double alpha, int accumulate) {
+  pdl_begin();
   extern __shared__ double fsm[];
   const FdSmall it = items[blockIdx.x];
   const int n0 = it.n0, n1 = it.n1;
@@ -644,6 +653,7 @@ __global__ void __launch_bounds__(256) fd_small_kernel(const FdSmall* __restrict
 __global__ void __launch_bounds__(256) piece_gemv_kernel(const PieceRowBlock* __restrict__ blocks,
                                                          const double* __restrict__ r, double* u,
                                                          double tau, int accumulate) {
+  pdl_begin();
   const PieceRowBlock b = blocks[blockIdx.x];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (warp >= b.nrows) return;
@@ -665,6 +675,7 @@ __global__ void __launch_bounds__(256) dot_kernel(int n, const double* __restric
                                                   const double* __restrict__ b, double* partials,
                                                   unsigned* counter, CgScalars* sc, int kind,
                                                   double* hist) {
+  pdl_begin();
   __shared__ double red[32];
   if (kind != FIN_NORMB && sc->done) return;
   double acc = 0.0;
@@ -680,6 +691,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int n, double* __restric
                                                         const double* __restrict__ q,
                                                         double* partials, unsigned* counter,
                                                         CgScalars* sc, double* hist) {
+  pdl_begin();
   __shared__ double red[32];
   if (sc->done) return;
   const double alpha = sc->alpha;
@@ -697,6 +709,7 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int n, double* __restric
 __global__ void __launch_bounds__(256) cg_direction_kernel(int n, double* __restrict__ d,
                                                            const double* __restrict__ z,
                                                            const CgScalars* sc) {
+  pdl_begin();
   if (sc->done) return;
   const double beta = sc->beta;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -707,6 +720,7 @@ __global__ void __launch_bounds__(256) cg_direction_kernel(int n, double* __rest
 // at all (||b|| != 0, max_iters > 0); else: continue after this iteration's update.
 __global__ void cg_cond_kernel(cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
                                const CgScalars* sc, int max_iters, int start) {
+  pdl_begin();
   if (threadIdx.x != 0) return;
   const unsigned cont = start ? (sc->normb != 0.0 && max_iters > 0) : (!sc->done && sc->it < max_iters);
   cudaGraphSetConditional(loop, cont);
@@ -714,11 +728,13 @@ __global__ void cg_cond_kernel(cudaGraphConditionalHandle loop, cudaGraphConditi
 }
 
 __global__ void copy_kernel(int n, double* __restrict__ dst, const double* __restrict__ src) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = src[i];
 }
 
 __global__ void fill_kernel(int n, double* __restrict__ dst, double v) {
+  pdl_begin();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     dst[i] = v;
 }
@@ -742,10 +758,10 @@ void launch_spmv(cudaStream_t s, int n, const int* ptr, const int* col, const do
   const long long threads = (long long)n * group;
   const int grid = blocks_for(threads, bs);
   switch (group) {
-    case 4: spmv_kernel<4><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
-    case 8: spmv_kernel<8><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
-    case 16: spmv_kernel<16><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
-    default: spmv_kernel<32><<<grid, bs, 0, s>>>(n, ptr, col, val, x, z, y, sign); break;
+    case 4: launch_k(spmv_kernel<4>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, x, z, y, sign); break;
+    case 8: launch_k(spmv_kernel<8>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, x, z, y, sign); break;
+    case 16: launch_k(spmv_kernel<16>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, x, z, y, sign); break;
+    default: launch_k(spmv_kernel<32>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, x, z, y, sign); break;
   }
 }
 
@@ -756,17 +772,17 @@ void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, cons
   long long g = ((long long)n * group + bs - 1) / bs;  // one row group per thread group
   const int grid = (int)(g < 1 ? 1 : (g > REDUCTION_MAX_BLOCKS ? REDUCTION_MAX_BLOCKS : g));
   switch (group) {
-    case 4: spmv_dot_kernel<4><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
-    case 8: spmv_dot_kernel<8><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
-    case 16: spmv_dot_kernel<16><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
-    default: spmv_dot_kernel<32><<<grid, bs, 0, s>>>(n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    case 4: launch_k(spmv_dot_kernel<4>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    case 8: launch_k(spmv_dot_kernel<8>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    case 16: launch_k(spmv_dot_kernel<16>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, d, q, partials, counter, sc, hist); break;
+    default: launch_k(spmv_dot_kernel<32>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, d, q, partials, counter, sc, hist); break;
   }
 }
 
 void launch_sptrsv(cudaStream_t s, const TrsvPhase& a, const TrsvPhase* b, int n_out,
                    const int* out_idx, double* out) {
   TrsvPhase bb = b ? *b : a;
-  sptrsv_kernel<<<1, 1024, 0, s>>>(a, bb, b ? 1 : 0, n_out, out_idx, out);
+  launch_k(sptrsv_kernel, dim3(1), dim3(1024), 0, s, a, bb, b ? 1 : 0, n_out, out_idx, out);
 }
 
 void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, double* out) {
@@ -780,9 +796,9 @@ void launch_coarse_csc(cudaStream_t s, const CoarseCsc& c, const double* rhs, do
   const size_t base = 24 * (size_t)c.n + 8 * ((size_t)c.n + 1);
   const size_t resident = base + 12 * ((size_t)c.lnnz + (size_t)c.unnz);
   if (resident <= 220 * 1024)
-    coarse_csc_kernel<true><<<1, threads < 32 ? 32 : threads, resident, s>>>(c, rhs, out);
+    launch_k(coarse_csc_kernel<true>, dim3(1), dim3(threads < 32 ? 32 : threads), resident, s, c, rhs, out);
   else
-    coarse_csc_kernel<false><<<1, threads < 32 ? 32 : threads, base, s>>>(c, rhs, out);
+    launch_k(coarse_csc_kernel<false>, dim3(1), dim3(threads < 32 ? 32 : threads), base, s, c, rhs, out);
 }
 
 // One shared-memory carveout for every kernel of the solve: the sweep and FD kernels
@@ -827,8 +843,8 @@ void level_prepare() {
 void launch_level_sweep(cudaStream_t s, const LevelArgs& a) {
   const size_t smem = level_smem_bytes(a);
   if (a.cluster <= 1) {
-    if (a.has_old) level_sweep_kernel<true, false><<<1, LEVEL_NT, smem, s>>>(a);
-    else level_sweep_kernel<false, false><<<1, LEVEL_NT, smem, s>>>(a);
+    if (a.has_old) launch_k(level_sweep_kernel<true, false>, dim3(1), dim3(LEVEL_NT), smem, s, a);
+    else launch_k(level_sweep_kernel<false, false>, dim3(1), dim3(LEVEL_NT), smem, s, a);
     return;
   }
   cudaLaunchConfig_t cfg = {};
@@ -836,29 +852,31 @@ void launch_level_sweep(cudaStream_t s, const LevelArgs& a) {
   cfg.blockDim = dim3(LEVEL_NT, 1, 1);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = a.cluster;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   if (a.has_old) cudaLaunchKernelEx(&cfg, level_sweep_kernel<true, true>, a);
   else cudaLaunchKernelEx(&cfg, level_sweep_kernel<false, true>, a);
 }
 
 void launch_perm_gather(cudaStream_t s, int n, const int* rows, const double* in, double* out) {
-  perm_gather_kernel<<<reduction_grid(n), 256, 0, s>>>(n, rows, in, out);
+  launch_k(perm_gather_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, rows, in, out);
 }
 
 void launch_perm_scatter(cudaStream_t s, int n, const int* rows, const double* xp, double* u, int accumulate) {
-  perm_scatter_kernel<<<reduction_grid(n), 256, 0, s>>>(n, rows, xp, u, accumulate);
+  launch_k(perm_scatter_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, rows, xp, u, accumulate);
 }
 
 void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,
                     const double* gsrc, double* sdst, double alpha, int accumulate) {
   if (total_tiles <= 0) return;
-  fd_gemm_kernel<<<total_tiles, 256, 0, s>>>(d_descs, ndesc, gsrc, sdst, alpha, accumulate);
+  launch_k(fd_gemm_kernel, dim3(total_tiles), dim3(256), 0, s, d_descs, ndesc, gsrc, sdst, alpha, accumulate);
 }
 
 void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
@@ -870,43 +888,43 @@ void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nma
     attr = true;
   }
   const size_t smem = sizeof(double) * (size_t)(4 * nmax * nmax);
-  fd_small_kernel<<<nitems, 256, smem, s>>>(d_items, r, u, alpha, accumulate);
+  launch_k(fd_small_kernel, dim3(nitems), dim3(256), smem, s, d_items, r, u, alpha, accumulate);
 }
 
 void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
                        const double* r, double* u, double tau, int accumulate) {
   if (nblocks <= 0) return;
-  piece_gemv_kernel<<<nblocks, 256, 0, s>>>(d_blocks, r, u, tau, accumulate);
+  launch_k(piece_gemv_kernel, dim3(nblocks), dim3(256), 0, s, d_blocks, r, u, tau, accumulate);
 }
 
 void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double* partials,
                 unsigned* counter, CgScalars* sc, int kind, double* hist) {
-  dot_kernel<<<reduction_grid(n), 256, 0, s>>>(n, a, b, partials, counter, sc, kind, hist);
+  launch_k(dot_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, a, b, partials, counter, sc, kind, hist);
 }
 
 void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double* d,
                       const double* q, double* partials, unsigned* counter, CgScalars* sc,
                       double* hist) {
-  cg_update_kernel<<<reduction_grid(n), 256, 0, s>>>(n, x, r, d, q, partials, counter, sc, hist);
+  launch_k(cg_update_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, x, r, d, q, partials, counter, sc, hist);
 }
 
 void launch_cg_cond(cudaStream_t s, cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
                     const CgScalars* sc, int max_iters, int start) {
-  cg_cond_kernel<<<1, 32, 0, s>>>(loop, more, sc, max_iters, start);
+  launch_k(cg_cond_kernel, dim3(1), dim3(32), 0, s, loop, more, sc, max_iters, start);
 }
 
 void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc) {
-  cg_direction_kernel<<<reduction_grid(n), 256, 0, s>>>(n, d, z, sc);
+  launch_k(cg_direction_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, d, z, sc);
 }
 
 void launch_copy(cudaStream_t s, int n, double* dst, const double* src) {
   if (n <= 0) return;
-  copy_kernel<<<reduction_grid(n), 256, 0, s>>>(n, dst, src);
+  launch_k(copy_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, dst, src);
 }
 
 void launch_fill(cudaStream_t s, int n, double* dst, double v) {
   if (n <= 0) return;
-  fill_kernel<<<reduction_grid(n), 256, 0, s>>>(n, dst, v);
+  launch_k(fill_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, dst, v);
 }
 
 }  // namespace igb

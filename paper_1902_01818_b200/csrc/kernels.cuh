@@ -11,7 +11,40 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 namespace igb {
+
+// Programmatic dependent launch: every kernel of the solve is launched with the
+// programmatic-serialization attribute and begins with pdl_begin() (griddepcontrol.wait:
+// the predecessor grid has completed and its writes are visible; then allow the next
+// kernel to be scheduled).  The successor's launch and ramp-up overlap this kernel's tail
+// instead of a full drain between dependent kernels.  IGB_PDL=0 disables the attribute.
+inline bool pdl_enabled() {
+  static const bool on = !(std::getenv("IGB_PDL") && std::atoi(std::getenv("IGB_PDL")) == 0);
+  return on;
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+#endif
+template <class... KArgs, class... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                            Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Same preferred shared-memory carveout for every kernel (kernels.cu).
 void carveout_prepare();

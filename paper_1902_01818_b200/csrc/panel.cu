@@ -175,6 +175,7 @@ __host__ __device__ constexpr int panel_warps() { return KBC == 17 ? 16 : 8; }
 
 template <int KBC, int KA, int KF>
 __global__ void __launch_bounds__(panel_warps<KBC>() * 32, 1) panel_sweep_kernel(PanelArgs a) {
+  pdl_begin();
   using Set = PanelSet<KA, KF>;
   extern __shared__ __align__(128) double psm[];
   constexpr int W = panel_warps<KBC>();
@@ -426,13 +427,15 @@ void launch_one(cudaStream_t st, const PanelArgs& a) {
   cfg.blockDim = dim3(panel_warps<KBC>() * 32, 1, 1);
   cfg.dynamicSmemBytes = panel_smem_bytes(a);
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = a.G;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   cudaLaunchKernelEx(&cfg, kern, a);
 }
 

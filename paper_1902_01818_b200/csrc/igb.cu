@@ -573,10 +573,12 @@ int guarded(igb_ctx* ctx, F&& f) {
 
 int pick_group(long long nnz, int n) {
   const double avg = n ? double(nnz) / n : 0;
+  static const int forced = std::getenv("IGB_SPMV_GROUP") ? std::atoi(std::getenv("IGB_SPMV_GROUP")) : 0;
+  if (forced == 4 || forced == 8 || forced == 16 || forced == 32) return forced;
+  // measured on B200 (cfg2, 48 nnz/row): 8 lanes per row beats 16 and 32 -- more independent
+  // loads per lane, fewer latency-bound waves of warps
   if (avg <= 6) return 4;
-  if (avg <= 14) return 8;
-  if (avg <= 40) return 16;
-  return 32;
+  return 8;
 }
 
 void check_csr(int n, int m, long long nnz, const int* ptr, const int* idx) {

@@ -11,7 +11,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --
   --log-file $O/launches_$TAG.csv python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_list_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:panel_sweep -s 40 -c 1 \
   -o $O/prof_gs_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_gs_$TAG.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fd_cluster -s 20 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:fd_back -s 20 -c 1 \
   -o $O/prof_fd_$TAG -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline > $O/ncu_fd_$TAG.log 2>&1
 tail -1 $O/bench_$TAG.log | cut -c1-200
 tail -1 $O/bench_ref_$TAG.log | cut -c1-200

@@ -10,11 +10,10 @@
 //   fd_back    3  B' = T0 A            left T0[rows, :]     right A (scratch, L2)
 //              4  X  = B' T1^T         left B' (own rows)   right T1^T    -> u[idx] (+)= alpha X
 //
-// Every CTA owns RB rows of one interior (all interiors of a level in one grid, ~2 CTAs
+// Every CTA owns RB rows of one interior (all interiors of a level in one grid, ~1 CTA
 // per SM) and thread j owns column j.  Left operands live in shared memory as [m][i] (RB
-// doubles per m: broadcast loads feeding RB FMAs of the thread's column); right operands
-// stream through a double-buffered [FDC_KC][FDC_NMAX] shared chunk, loaded into
-// registers one chunk ahead.
+// doubles per m: broadcast loads feeding RB FMAs of the thread's column); each product's
+// right operand is copied whole into shared memory by cp.async (one latency per product).
 #include <cuda_runtime.h>
 
 #include "kernels.cuh"
@@ -23,19 +22,21 @@ namespace igb {
 
 namespace {
 
-constexpr int FDC_KC = 16;  // right-operand rows per chunk
+constexpr int FDC_KC = 16;  // gathered-operand rows per chunk
 
 template <int RB>
-constexpr size_t fd_smem() {
-  return 8 * (2 * (size_t)FDC_NMAX * RB + 2 * (size_t)FDC_KC * FDC_NMAX);
+size_t fd_smem(int kmax) {
+  // right-operand buffer: whole operand (kmax rows) or the two gather chunks, whichever is larger
+  return 8 * (2 * (size_t)FDC_NMAX * RB + (size_t)(kmax > 2 * FDC_KC ? kmax : 2 * FDC_KC) * FDC_NMAX);
 }
 
-// acc[i] = sum_m L[m][i] * Rt(m, j) for m < K; the right operand streams through two shared
-// chunks, each thread loading its column of the next chunk into registers while the
-// current one is multiplied.
+// Gathered right operand (R = r[idx], step 1): 16-row chunks, each thread loading its column
+// of the next chunk into registers while the current one is multiplied (plain loads; 8-byte
+// cp.async copies of a gather measured slower).  rch: two [FDC_KC][FDC_NMAX] chunks.
 template <int RB, class Load>
-__device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB], int K, int j,
-                                         double (*rch)[FDC_KC][FDC_NMAX], Load ld) {
+__device__ __forceinline__ void fdc_gemm_chunked(double (&acc)[RB], const double (*L)[RB], int K, int j,
+                                                 double* rch_base, Load ld) {
+  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(rch_base);
 #pragma unroll
   for (int i = 0; i < RB; ++i) acc[i] = 0.0;
   double pre[FDC_KC];
@@ -54,22 +55,43 @@ __device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB
     }
     const int m0 = q * FDC_KC;
     const int kn = min(FDC_KC, K - m0);
-    if (kn == FDC_KC) {
+    for (int k = 0; k < kn; ++k) {
+      const double x = buf[k][j];
+      const double* l = L[m0 + k];
 #pragma unroll
-      for (int k = 0; k < FDC_KC; ++k) {
-        const double x = buf[k][j];
-        const double* l = L[m0 + k];
-#pragma unroll
-        for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], x, acc[i]);
-      }
-    } else {
-      for (int k = 0; k < kn; ++k) {
-        const double x = buf[k][j];
-        const double* l = L[m0 + k];
-#pragma unroll
-        for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], x, acc[i]);
-      }
+      for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], x, acc[i]);
     }
+  }
+}
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((unsigned)__cvta_generic_to_shared(dst)), "l"(src)
+               : "memory");
+}
+
+// acc[i] = sum_m L[m][i] * Rt(m, j) for m < K.  The whole right operand is copied into the
+// shared buffer Rs ([m][FDC_NMAX]) at once -- every thread issues cp.async for its column of
+// all K rows (8-byte copies, so gathered operands work too) -- one memory latency per product,
+// then the multiply runs from shared memory.  The caller synchronises before Rs is reused.
+template <int RB, class Addr>
+__device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB], int K, int j, bool active,
+                                         double* Rs, Addr addr) {
+  if (active) {
+#pragma unroll 4
+    for (int m = 0; m < K; ++m) cp_async8(Rs + m * FDC_NMAX + j, addr(m));
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < RB; ++i) acc[i] = 0.0;
+  const double* x = Rs + j;
+#pragma unroll 8
+  for (int m = 0; m < K; ++m) {
+    const double xm = x[m * FDC_NMAX];
+    const double* l = L[m];
+#pragma unroll
+    for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], xm, acc[i]);
   }
 }
 
@@ -121,19 +143,22 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_front_kernel(const __grid_consta
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
   double (*outT)[RB] = lop + FDC_NMAX;
-  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(fdc_smem + 2 * FDC_NMAX * RB);
+  double* Rs = fdc_smem + 2 * FDC_NMAX * RB;  // [kmax][FDC_NMAX] right operand
   const FdCtx c = fd_locate(bt);
   const int n1 = c.n1, jj = c.jj;
   double acc[RB];
   // 1: B = T0^T R
   fd_fill<RB>(lop, c, false);
   __syncthreads();
-  fdc_gemm<RB>(acc, lop, c.n0, c.j, rch, [&](int m) { return r[__ldg(c.it.idx + (size_t)m * n1 + jj)]; });
+  if (c.j == 0)  // step 2's operand: into L2 while step 1 runs
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.it.T1), "r"((unsigned)(8 * n1 * n1) & ~15u)
+                 : "memory");
+  fdc_gemm_chunked<RB>(acc, lop, c.n0, c.j, Rs, [&](int m) { return r[__ldg(c.it.idx + (size_t)m * n1 + jj)]; });
 #pragma unroll
   for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
   __syncthreads();
   // 2: A = (B T1) ./ D    left outT[m][i] = B[i][m]
-  fdc_gemm<RB>(acc, outT, n1, c.j, rch, [&](int m) { return __ldg(c.it.T1 + (size_t)m * n1 + jj); });
+  fdc_gemm<RB>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)m * n1 + jj; });
   if (c.active) {
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -173,7 +198,7 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constan
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
   double (*outT)[RB] = lop + FDC_NMAX;
-  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(fdc_smem + 2 * FDC_NMAX * RB);
+  double* Rs = fdc_smem + 2 * FDC_NMAX * RB;  // [kmax][FDC_NMAX] right operand
   const FdCtx c = fd_locate(bt);
   const int n1 = c.n1, jj = c.jj;
   double acc[RB];
@@ -183,12 +208,12 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constan
 #pragma unroll
   for (int i = 0; i < RB; ++i) gi[i] = __ldg(c.it.idx + (size_t)(c.r0 + min(i, max(c.nr - 1, 0))) * n1 + jj);
   __syncthreads();
-  fdc_gemm<RB>(acc, lop, c.n0, c.j, rch, [&](int m) { return c.it.scratch[(size_t)m * n1 + jj]; });
+  fdc_gemm<RB>(acc, lop, c.n0, c.j, c.active, Rs, [&](int m) { return c.it.scratch + (size_t)m * n1 + jj; });
 #pragma unroll
   for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
   __syncthreads();
   // 4: X = B' T1^T       right T1[j][m]
-  fdc_gemm<RB>(acc, outT, n1, c.j, rch, [&](int m) { return __ldg(c.it.T1 + (size_t)jj * n1 + m); });
+  fdc_gemm<RB>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)jj * n1 + m; });
   if (c.active) {
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -203,20 +228,21 @@ template <int RB>
 void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fd_front_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>());
-    cudaFuncSetAttribute(fd_back_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>());
+    cudaFuncSetAttribute(fd_front_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>(FDC_NMAX));
+    cudaFuncSetAttribute(fd_back_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>(FDC_NMAX));
     attr = true;
   }
   const int grid = bt.cta0[bt.nitems];
-  launch_k(fd_front_kernel<RB>, dim3(grid), dim3(FDC_NT), fd_smem<RB>(), s, bt, r);
-  launch_k(fd_back_kernel<RB>, dim3(grid + bt.npieces), dim3(FDC_NT), fd_smem<RB>(), s, bt, r, u, alpha, accumulate);
+  const size_t smem = fd_smem<RB>(bt.kmax);
+  launch_k(fd_front_kernel<RB>, dim3(grid), dim3(FDC_NT), smem, s, bt, r);
+  launch_k(fd_back_kernel<RB>, dim3(grid + bt.npieces), dim3(FDC_NT), smem, s, bt, r, u, alpha, accumulate);
 }
 
 }  // namespace
 
 int fd_rows_per_cta(int total_rows) {
-  // about two CTAs per SM for the level's interiors together
-  const int want = (total_rows + 295) / 296;
+  // about one CTA per SM for the level's interiors together (the right operand fills shared memory)
+  const int want = (total_rows + 147) / 148;
   return want <= 2 ? 2 : (want <= 4 ? 4 : 8);
 }
 

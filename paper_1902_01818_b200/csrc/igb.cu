@@ -699,6 +699,8 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
         bytes += 16.0 * (n0 * n0 + n1 * n1) + (12.0 + 8 + 16 + 12) * n0 * n1;
       }
       bt.rb = fd_rows_per_cta(rows);
+      bt.kmax = 1;
+      for (int i = 0; i < bt.nitems; ++i) bt.kmax = std::max(bt.kmax, std::max(bt.items[i].n0, bt.items[i].n1));
       bt.cta0[0] = 0;
       for (int i = 0; i < bt.nitems; ++i) bt.cta0[i + 1] = bt.cta0[i] + (bt.items[i].n0 + bt.rb - 1) / bt.rb;
       V.fd.batches.push_back(bt);

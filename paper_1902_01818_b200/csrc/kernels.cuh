@@ -211,6 +211,7 @@ struct FdBatch {
   int cta0[FD_BATCH_MAX + 1];  // first CTA of each item; cta0[nitems] = grid size
   int nitems;
   int rb;                      // rows per CTA: 2, 4 or 8
+  int kmax;                    // largest n0 / n1 of the batch (shared-memory buffer rows)
   const PieceRowBlock* pieces; // interface-piece rows (<= 5 per block) done by extra CTAs of
   int npieces;                 // the back kernel (disjoint u entries), or none
 };

@@ -22,6 +22,7 @@
 
 #include "igb.h"
 #include "level_plan.h"
+#include "flow_plan.h"
 #include "panel_plan.h"
 #include "kernels.cuh"
 
@@ -98,6 +99,14 @@ struct PanelDev {
   double lin_bytes = 0, ent_bytes = 0;
 };
 
+struct FlowDev {
+  bool ok = false;
+  FlowArgs args{};
+  std::vector<int> h_row, h_qlev;  // kept for IGB_FLOW_TRACE dumps
+  int nlev = 0;
+  long long entries = 0;
+};
+
 struct Level {
   int n = 0;
   DevCsr A;
@@ -105,6 +114,7 @@ struct Level {
   std::vector<double> h_val;
   SweepDev sweep[2];   // 0: forward (lower) sweep, 1: backward (upper) sweep
   PanelDev panel[2];   // row-panel sweeps (preferred when built)
+  FlowDev flow[2];     // dependency-driven whole-GPU sweeps (wide levels, long rows)
   double* xg = nullptr;  // panel sweep solution by position (old values)
   double* rp = nullptr;   // level-ordered right-hand side / solution of the sweep
   double* xp = nullptr;
@@ -330,6 +340,55 @@ struct igb_ctx {
                      l, upper ? 1 : 0, V.n, hd[0], hd[1] / np, hd[2] / np, hd[3] / np, hd[4] / np, hd[5] / np,
                      hd[6] / np, hd[7] / np);
       }
+      return;
+    }
+    FlowDev& Fw = V.flow[upper ? 1 : 0];
+    if (Fw.ok) {
+      FlowArgs a = Fw.args;
+      a.res = rhs;
+      a.u = u;
+      a.accumulate = u_zero ? 0 : 1;
+      const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
+      static const bool want_dbg = std::getenv("IGB_GS_DEBUG") != nullptr;
+      if (want_dbg && !capturing) {
+        cudaEvent_t e0, e1;
+        CU(cudaEventCreate(&e0));
+        CU(cudaEventCreate(&e1));
+        const char* tr = std::getenv("IGB_FLOW_TRACE");
+        long long* dtr = nullptr;
+        if (tr) {
+          CU(cudaMalloc(&dtr, 4 * sizeof(long long) * a.nq));
+          CU(cudaMemsetAsync(dtr, 0, 4 * sizeof(long long) * a.nq, stream));
+          a.trace = dtr;
+        }
+        CU(cudaEventRecord(e0, stream));
+        launch_flow_sweep(stream, a);
+        CU(cudaEventRecord(e1, stream));
+        CU(cudaEventSynchronize(e1));
+        if (tr) {  // binary dump: int nq, int[nq] row, int[nq] level, int64[4 nq] trace
+          std::vector<long long> ht(4 * (size_t)a.nq);
+          CU(cudaMemcpy(ht.data(), dtr, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+          cudaFree(dtr);
+          char path[512];
+          std::snprintf(path, sizeof(path), "%s.l%d.d%d.bin", tr, l, upper ? 1 : 0);
+          if (FILE* fp = std::fopen(path, "wb")) {
+            std::fwrite(&a.nq, sizeof(int), 1, fp);
+            std::fwrite(Fw.h_row.data(), sizeof(int), Fw.h_row.size(), fp);
+            std::fwrite(Fw.h_qlev.data(), sizeof(int), Fw.h_qlev.size(), fp);
+            std::fwrite(ht.data(), sizeof(long long), ht.size(), fp);
+            std::fclose(fp);
+          }
+        }
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        std::fprintf(stderr, "[gs dbg] flow level %d dir %d n %d depth %d ctas %d G %d: %.1f us, %.3f us/level\n", l,
+                     upper ? 1 : 0, V.n, Fw.nlev, a.ctas, a.G, ms * 1e3, ms * 1e3 / std::max(1, Fw.nlev));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return;
+      }
+      launch(K_GS, bytes, [&] { launch_flow_sweep(stream, a); });
       return;
     }
     SweepDev& C = V.sweep[upper ? 1 : 0];
@@ -1006,6 +1065,64 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
   return true;
 }
 
+double flow_min_width() {
+  static double w = -1;
+  if (w < 0) {
+    const char* e = std::getenv("IGB_FLOW_MIN_WIDTH");
+    w = e ? std::atof(e) : 96.0;
+  }
+  return w;
+}
+
+// Dependency-driven whole-GPU sweep for one direction (flow_plan.h, flow.cu).
+bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
+  const char* ge = std::getenv("IGB_FLOW_G");
+  FlowPlanHost plan;
+  const char* le = std::getenv("IGB_FLOW_CRITLAG");
+  if (!build_flow_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
+                       ge ? std::atoi(ge) : 0, le ? std::max(1, std::atoi(le)) : 2, plan))
+    return false;
+  FlowDev& F = V.flow[dir];
+  FlowArgs& a = F.args;
+  a = FlowArgs{};
+  a.n = V.n;
+  a.nq = plan.nq;
+  a.G = plan.G;
+  a.row = ctx->upload(plan.row.data(), plan.row.size());
+  a.eptr = ctx->upload(plan.eptr.data(), plan.eptr.size());
+  a.ecol = plan.entries ? ctx->upload(plan.ecol.data(), plan.ecol.size()) : ctx->alloc<int>(1);
+  a.eval = plan.entries ? ctx->upload(plan.eval.data(), plan.eval.size()) : ctx->alloc<double>(1);
+  a.idiag = ctx->upload(plan.idiag.data(), plan.idiag.size());
+  const char* ce = std::getenv("IGB_FLOW_CRIT");
+  if (!ce || std::atoi(ce)) a.crit = ctx->upload(plan.crit.data(), plan.crit.size());
+  const char* be = std::getenv("IGB_FLOW_BACKOFF");
+  a.backoff = be ? std::atoi(be) : 0;
+  std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF5678ULL);  // flow.cu FLOW_PENDING
+  a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
+  int* ctr = ctx->alloc<int>(2);
+  CU(cudaMemset(ctr, 0, 2 * sizeof(int)));
+  a.par_ctr = ctr;
+  a.done_ctr = reinterpret_cast<unsigned*>(ctr + 1);
+  // enough warps for ~inflight dependency levels at once (idle warps only poll L2)
+  const char* fe = std::getenv("IGB_FLOW_INFLIGHT");
+  const double inflight = fe ? std::atof(fe) : 8.0;
+  const double width = double(plan.nq) / std::max(1, plan.nlev);
+  const double warps = inflight * width / (32 / plan.G);
+  const int want = (int)std::ceil(warps / (FLOW_NT / 32));
+  a.ctas = std::max(1, std::min(flow_max_ctas(), want));
+  F.nlev = plan.nlev;
+  F.entries = plan.entries;
+  if (std::getenv("IGB_FLOW_TRACE")) {
+    F.h_row = plan.row;
+    F.h_qlev = plan.qlev;
+  }
+  F.ok = true;
+  if (std::getenv("IGB_VERBOSE"))
+    std::fprintf(stderr, "[igb] level %d dir %d: flow sweep n %d depth %d width %.0f entries %lld G %d ctas %d\n",
+                 level, dir, V.n, plan.nlev, width, plan.entries, plan.G, a.ctas);
+  return true;
+}
+
 int igb_set_gs(igb_ctx* ctx, int level) {
   return guarded(ctx, [&] {
     require_levels(ctx);
@@ -1036,6 +1153,17 @@ int igb_set_gs(igb_ctx* ctx, int level) {
         const Sched& Sd = dir ? V.bwd : V.fwd;
         panel_done[dir] = build_panel_sweep(ctx, V, level, dir, dp, Sd.nlev, engine == "panel");
       }
+    }
+    // whole-GPU dependency-driven sweep: wide dependency levels (3-D, high degree) where the
+    // panel chain is not short; IGB_GS_ENGINE=flow forces it on every level
+    for (int dir = 0; dir < 2; ++dir) {
+      if (panel_done[dir]) continue;
+      const Sched& Sd = dir ? V.bwd : V.fwd;
+      const double width = double(V.n) / std::max(1, Sd.nlev);
+      const long long tri = dir ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const bool want = engine == "flow" ||
+                        (engine == "auto" && (width >= flow_min_width() || tri >= 48LL * V.n));
+      if (want) panel_done[dir] = build_flow_sweep(ctx, V, level, dir, dp);
     }
     level_prepare();
     const char* clenv = std::getenv("IGB_GS_CLUSTER");

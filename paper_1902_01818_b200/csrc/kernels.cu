@@ -825,6 +825,7 @@ void carveout_prepare() {
   for (const void* f : funcs) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaGetLastError();
   set_carveout_panel_fd(pct);
+  flow_set_carveout(pct);
 }
 
 size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }

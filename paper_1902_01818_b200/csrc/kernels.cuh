@@ -137,6 +137,31 @@ bool panel_prepare(int G, int KBC);   // false: no cluster of G CTAs fits this d
 int panel_max_clusters(int G, int KBC, size_t smem);  // clusters of G CTAs co-resident
 void launch_panel_sweep(cudaStream_t s, const PanelArgs& a);
 
+// ---- dependency-driven triangular sweep over the whole GPU (flow.cu, flow_plan.h) ----
+// Rows in dependency-level order (list slot q -> row[q], -1 = padding), strict-triangle
+// entries of slot q at [eptr[q], eptr[q+1]) (ecol: row index, eval), idiag[q] = 1 / a_qq.
+// Solution values published in xg[par][row] (sentinel until produced; see flow.cu).
+constexpr int FLOW_NT = 256;
+struct FlowArgs {
+  const int* row;      // [nq]
+  const int* eptr;     // [nq + 1]
+  const int* ecol;
+  const double* eval;
+  const double* idiag; // [nq]
+  const double* res;   // right-hand side by row
+  double* u;           // u (+)= c by row
+  double* xg;          // [2][n]
+  int* par_ctr;        // sweep parity of this level and direction (device)
+  unsigned* done_ctr;  // CTAs finished (device), reset by the last one
+  int n, nq, G, ctas, accumulate;
+  const int* crit;     // nullable: [nq] the dependency of the highest level (polled first)
+  int backoff;         // ns slept between polls of crit (0: spin)
+  long long* trace;    // debug (nullable): per slot globaltimer at start / deps ready / stored
+};
+int flow_max_ctas();  // co-resident CTAs of FLOW_NT threads (all variants)
+void flow_set_carveout(int pct);
+void launch_flow_sweep(cudaStream_t s, const FlowArgs& a);
+
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
 // y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
 // out[i] = w[perm_c[i]].  Column j updates run in parallel; one barrier per column.

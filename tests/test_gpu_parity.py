@@ -228,3 +228,45 @@ def test_level_set_engine_still_matches_oracle():
     xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert rep.iterations == itso
     solver.close()
+
+
+FLOW_CASES = [("cfg2", {"levels": 3}, None), ("cfg3", {"levels": 2}, None), ("cfg5", {"levels": 2}, None),
+              ("cfg4", {"p": 4, "levels": 2}, "8"), ("cfg2", {"levels": 2}, "16")]
+
+
+@pytest.mark.parametrize("cfg,kw,G", FLOW_CASES)
+def test_flow_engine_matches_oracle(cfg, kw, G):
+    """IGB_GS_ENGINE=flow: the dependency-driven whole-GPU sweep on every level (chosen
+    automatically for wide levels: 3-D, high degree).  Each sweep 6x bitwise repeatable
+    (fixed per-row summation order, parity-alternating sentinel copy), within 1e-12 of
+    SuperLU on tril/triu, and the PCG solve matches the oracle."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup(cfg, **kw)
+    os.environ["IGB_GS_ENGINE"] = "flow"
+    if G:
+        os.environ["IGB_FLOW_G"] = G
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_GS_ENGINE"]
+        os.environ.pop("IGB_FLOW_G", None)
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(23)
+    for level in range(1, solver.finest + 1):
+        if orc.gs[level] is None:
+            continue
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for op, ref in (("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward)):
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(5):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (cfg, level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (cfg, level, op)
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, "flow vs oracle")
+    assert rel(rep.x, xo) <= 1e-10
+    solver.close()

@@ -637,7 +637,8 @@ int pick_group(long long nnz, int n) {
   // measured on B200 (cfg2, 48 nnz/row): 8 lanes per row beats 16 and 32 -- more independent
   // loads per lane, fewer latency-bound waves of warps
   if (avg <= 6) return 4;
-  return 8;
+  if (avg <= 96) return 8;
+  return avg <= 192 ? 16 : 32;  // long rows (3-D, p = 8): more lanes per row
 }
 
 void check_csr(int n, int m, long long nnz, const int* ptr, const int* idx) {

@@ -87,6 +87,31 @@ __device__ void finish_reduction(double blocksum, double* partials, unsigned* co
 
 // ---------------------------------------------------------------------------
 // CSR SpMV
+// Row dot product for one lane of a G-lane row group: entries k = b + lane, b + lane + G, ...
+// summed in that order (one accumulator), loads issued four entries ahead for memory-level
+// parallelism on long rows (3-D, high degree).
+template <int G>
+__device__ __forceinline__ double row_dot(int b, int e, int lane, const int* __restrict__ col,
+                                          const double* __restrict__ val, const double* __restrict__ x) {
+  double s = 0.0;
+  int k = b + lane;
+  for (; k + 3 * G < e; k += 4 * G) {
+    int c[4];
+    double v[4], xv[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      c[j] = __ldg(&col[k + j * G]);
+      v[j] = __ldg(&val[k + j * G]);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) xv[j] = __ldg(&x[c[j]]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s = fma(v[j], xv[j], s);
+  }
+  for (; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&x[__ldg(&col[k])]), s);
+  return s;
+}
+
 template <int G>
 __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict__ ptr,
                                                    const int* __restrict__ col,
@@ -100,7 +125,7 @@ __global__ void __launch_bounds__(256) spmv_kernel(int n, const int* __restrict_
   double s = 0.0;
   if (row < n) {
     const int b = __ldg(&ptr[row]), e = __ldg(&ptr[row + 1]);
-    for (int k = b + lane; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&x[__ldg(&col[k])]), s);
+    s = row_dot<G>(b, e, lane, col, val, x);
   }
 #pragma unroll
   for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -130,7 +155,7 @@ __global__ void __launch_bounds__(256) spmv_dot_kernel(int n, const int* __restr
     double s = 0.0;
     if (row < n) {
       const int b = __ldg(&ptr[row]), e = __ldg(&ptr[row + 1]);
-      for (int k = b + lane; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&d[__ldg(&col[k])]), s);
+      s = row_dot<G>(b, e, lane, col, val, d);
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);

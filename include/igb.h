@@ -10,6 +10,8 @@
  *                             (reference pkg/src/igamg/multigrid.py:92-99)
  *   igb_set_prolongation   <- assembly.prolongation / self.P[l]
  *                             (assembly.py:672-702, multigrid.py:96)
+ *   igb_set_prolongation_kron <- the same P in per-patch Kronecker form
+ *                             (assembly.py:672-702, bspline.py:233-246)
  *   igb_set_gs             <- smoothers.GaussSeidel.__init__ (smoothers.py:174-184)
  *   igb_scms_add_interior  <- smoothers.ScmsInteriorSolver.__init__ (smoothers.py:232-281)
  *   igb_scms_add_piece     <- SubspaceCorrectedMass piece factorizations (smoothers.py:316-319)
@@ -80,6 +82,21 @@ int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz,
 /* P_l (l = 1..L): n_l x n_{l-1} CSR; the transpose for restriction is built here. */
 int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long long nnz,
                          const int* indptr, const int* indices, const double* data);
+
+/* Kronecker form of P_l (replaces assembly.prolongation's assembled matrix on the device,
+ * assembly.py:672-702: per patch the kron of bspline.two_scale_refine 1-D matrices,
+ * bspline.py:233-246, mapped to free DoFs with shared rows assigned once).  With
+ * IGB_TRANSFER=kron in the environment restriction and prolongation on level l use it; by
+ * default the CSR pair of igb_set_prolongation runs (measured faster on B200 at the BASELINE
+ * sizes).  Needs both level matrices set.
+ *   nf, nc      [npatch * dim] per-patch block sizes per axis, fine / coarse level
+ *   p1_idx/val  the 1-D matrices P_{k,a} (patch-major, then axis), each n_f,a rows of
+ *               `width` ELL entries, columns ascending, -1 = padding
+ *   fine_free   [sum_k prod nf] block index -> free id (-1 Dirichlet); coarse_free likewise
+ *   fine_owner  [sum_k prod nf] 1 where the block copy is its DoF class root, else 0 */
+int igb_set_prolongation_kron(igb_ctx* ctx, int level, int dim, int npatch, const int* nf, const int* nc,
+                              int width, const int* p1_idx, const double* p1_val, const int* fine_free,
+                              const int* fine_owner, const int* coarse_free);
 
 /* Gauss-Seidel on A_l in natural order (level schedules are built here). */
 int igb_set_gs(igb_ctx* ctx, int level);

@@ -31,6 +31,7 @@ SIGNATURES = {
     "igb_set_num_levels": ([_p, _i], _i),
     "igb_set_level_matrix": ([_p, _i, _i, _ll, _p, _p, _p], _i),
     "igb_set_prolongation": ([_p, _i, _i, _i, _ll, _p, _p, _p], _i),
+    "igb_set_prolongation_kron": ([_p, _i, _i, _i, _p, _p, _i, _p, _p, _p, _p, _p], _i),
     "igb_set_gs": ([_p, _i], _i),
     "igb_scms_begin": ([_p, _i, _d], _i),
     "igb_scms_add_interior": ([_p, _i, _i, _p, _p, _p, _p, _p, _p], _i),
@@ -133,6 +134,16 @@ class Context:
         p, i, v = self._csr_arrays(P)
         self._check(self.lib.igb_set_prolongation(self.h, level, P.shape[0], P.shape[1], len(v),
                                                   _ptr(p), _ptr(i), _ptr(v)), "igb_set_prolongation")
+
+    def set_prolongation_kron(self, level, kd):
+        """Kronecker form of P_level (assembly.prolongation_kron)."""
+        arrs = [_c(kd[k], np.int32) for k in ("nf", "nc", "idx")] + [_c(kd["val"], np.float64)] + \
+               [_c(kd[k], np.int32) for k in ("fine_free", "fine_owner", "coarse_free")]
+        nf, nc, idx, val, ff, fo, cf = arrs
+        self._check(self.lib.igb_set_prolongation_kron(self.h, level, int(kd["dim"]), int(kd["nf"].shape[0]),
+                                                       _ptr(nf), _ptr(nc), int(kd["width"]), _ptr(idx), _ptr(val),
+                                                       _ptr(ff), _ptr(fo), _ptr(cf)),
+                    "igb_set_prolongation_kron")
 
     def set_gs(self, level):
         self._check(self.lib.igb_set_gs(self.h, level), "igb_set_gs")

@@ -811,3 +811,92 @@ def prolongation(hier, level):
     key = r * np.int64(dofs_c.n_free) + c
     _, first = np.unique(key, return_index=True)
     return scipy.sparse.csr_matrix((v[first], (r[first], c[first])), shape=(dofs_f.n_free, dofs_c.n_free))
+
+
+def prolongation_kron(hier, level):
+    """Kronecker description of ``prolongation(hier, level)`` for the device transfer.
+
+    The reference builds P per patch as the Kronecker product of 1-D two-scale matrices and
+    maps it to free DoFs, assigning (not summing) the rows of shared interface DoFs
+    (``assembly.py:672-702``).  Returned here instead of the assembled CSR:
+
+    * ``nf``, ``nc``: int32 [npatch, dim] per-patch block sizes of the fine / coarse level;
+    * ``idx``, ``val``: the 1-D matrices P_{k,a} (patch-major, then axis) as ELL rows of
+      ``width`` entries (column -1 = padding), row-major;
+    * ``fine_free`` / ``coarse_free``: block index -> free id (-1: Dirichlet);
+    * ``fine_owner``: 1 where the fine block copy is its class root -- the one copy a
+      restriction may read, so that shared rows are counted once as in P^T.
+    """
+    if level < 1:
+        raise ValueError("prolongation needs level >= 1")
+    dofs_f, dofs_c = hier.dofs[level], hier.dofs[level - 1]
+    npatch = hier.domain.num_patches
+    dim = len(hier.spaces[level][0])
+    mats = []
+    for k in range(npatch):
+        for sc, sf in zip(hier.spaces[level - 1][k], hier.spaces[level][k]):
+            if sc == sf:
+                mats.append(scipy.sparse.identity(sc.n, format="csr"))
+            else:
+                refined, P1 = bs.two_scale_refine(sc)
+                if refined != sf:
+                    raise AssertionError("hierarchy spaces are not dyadically nested")
+                mats.append(scipy.sparse.csr_matrix(P1))
+    width = max(int(np.diff(m.indptr).max()) for m in mats)
+    idx, val = [], []
+    for m in mats:
+        m = scipy.sparse.csr_matrix(m)
+        m.sort_indices()
+        n = m.shape[0]
+        cnt = np.diff(m.indptr)
+        slot = np.arange(m.nnz) - np.repeat(m.indptr[:-1], cnt)
+        rows = np.repeat(np.arange(n), cnt)
+        i2 = np.full((n, width), -1, dtype=np.int32)
+        v2 = np.zeros((n, width))
+        i2[rows, slot] = m.indices
+        v2[rows, slot] = m.data
+        idx.append(i2.ravel())
+        val.append(v2.ravel())
+    nf = np.array([dofs_f.dims[k] for k in range(npatch)], dtype=np.int32).reshape(npatch, dim)
+    nc = np.array([dofs_c.dims[k] for k in range(npatch)], dtype=np.int32).reshape(npatch, dim)
+    return dict(dim=dim, nf=nf, nc=nc, width=width,
+                idx=np.concatenate(idx).astype(np.int32), val=np.concatenate(val),
+                fine_free=dofs_f.free_of_block.astype(np.int32),
+                fine_owner=(dofs_f.class_of == np.arange(dofs_f.n_block)).astype(np.int32),
+                coarse_free=dofs_c.free_of_block.astype(np.int32),
+                n_fine=dofs_f.n_free, n_coarse=dofs_c.n_free)
+
+
+def kron_apply(kd, x, transpose=False):
+    """Host restatement of the device Kronecker transfer (test check): P x, or P^T x."""
+    dim, npatch = kd["dim"], kd["nf"].shape[0]
+    out = np.zeros(kd["n_coarse"] if transpose else kd["n_fine"])
+    width = kd["width"]
+    pos = 0
+    offf = np.concatenate([[0], np.cumsum(np.prod(kd["nf"], axis=1))])
+    offc = np.concatenate([[0], np.cumsum(np.prod(kd["nc"], axis=1))])
+    for k in range(npatch):
+        ops = []
+        for a in range(dim):
+            n_f, n_c = int(kd["nf"][k, a]), int(kd["nc"][k, a])
+            i2 = kd["idx"][pos: pos + n_f * width].reshape(n_f, width)
+            v2 = kd["val"][pos: pos + n_f * width].reshape(n_f, width)
+            pos += n_f * width
+            rows = np.repeat(np.arange(n_f), width)
+            m = i2.ravel() >= 0
+            ops.append(scipy.sparse.csr_matrix((v2.ravel()[m], (rows[m], i2.ravel()[m])), shape=(n_f, n_c)))
+        Pk = _kron_chain(ops)
+        ff = kd["fine_free"][offf[k]:offf[k + 1]]
+        cf = kd["coarse_free"][offc[k]:offc[k + 1]]
+        if transpose:
+            own = kd["fine_owner"][offf[k]:offf[k + 1]].astype(bool) & (ff >= 0)
+            r = np.zeros(len(ff))
+            r[own] = x[ff[own]]
+            z = Pk.T @ r
+            np.add.at(out, cf[cf >= 0], z[cf >= 0])
+        else:
+            e = np.where(cf >= 0, x[np.maximum(cf, 0)], 0.0)
+            y = Pk @ e
+            own = kd["fine_owner"][offf[k]:offf[k + 1]].astype(bool) & (ff >= 0)
+            out[ff[own]] = y[own]
+    return out

@@ -122,6 +122,8 @@ struct Level {
   int* dpos = nullptr;
   bool has_P = false;
   DevCsr P, PT;
+  bool has_kron = false;  // Kronecker form of P (transfer.cu), used instead of the CSR pair
+  KronArgs kron{};
   bool has_gs = false;
   bool has_U = false;
   DevCsr U;  // strict upper triangle of A: residual after a forward sweep from zero is -U c
@@ -303,6 +305,28 @@ struct igb_ctx {
   void spmv(const DevCsr& M, const double* x_, const double* z, double* y, int sign, int cls) {
     const double bytes = 12.0 * M.nnz + 4.0 * (M.n + 1) + 8.0 * M.m + 8.0 * M.n + (sign ? 8.0 * M.n : 0.0);
     launch(cls, bytes, [&] { launch_spmv(stream, M.n, M.ptr, M.col, M.val, x_, z, y, sign, M.group); });
+  }
+
+  // y = P_l e (accumulate: y = z + P_l e) and y = P_l^T r, Kronecker form when set
+  void prolong(int l, const double* e, const double* z, double* y, int accumulate) {
+    Level& V = lev[l];
+    if (V.has_kron) {
+      const KronArgs& k = V.kron;
+      const double bytes = (16.0 + (accumulate ? 8.0 : 0.0)) * k.n_fine + 12.0 * k.n_coarse;
+      launch(K_TRANSFER, bytes, [&] { launch_kron_prolong(stream, k, e, z, y, accumulate); });
+      return;
+    }
+    spmv(V.P, e, accumulate ? z : nullptr, y, accumulate ? 1 : 0, K_TRANSFER);
+  }
+  void restrict_to(int l, const double* r, double* y) {
+    Level& V = lev[l];
+    if (V.has_kron) {
+      const KronArgs& k = V.kron;
+      const double bytes = 12.0 * k.n_fine + 16.0 * k.n_coarse;
+      launch(K_TRANSFER, bytes, [&] { launch_kron_restrict(stream, k, r, y); });
+      return;
+    }
+    spmv(V.PT, r, nullptr, y, 0, K_TRANSFER);
   }
 
   // GS correction on level l: solve tril (fwd) / triu (bwd); if into_u_zero the
@@ -550,7 +574,7 @@ struct igb_ctx {
       residual(l, f, u, V.r);
       res = V.r;
     }
-    spmv(V.PT, res, nullptr, fc, 0, K_TRANSFER);
+    restrict_to(l, res, fc);
   }
 
   // cycle on level l: f -> u (u overwritten)
@@ -562,12 +586,12 @@ struct igb_ctx {
     restrict_residual(l, f, u, uz, C.f);
     if (l == 1) {
       coarse_solve(C.f, C.u);
-      spmv(V.P, C.u, uz ? nullptr : u, u, uz ? 0 : 1, K_TRANSFER);
+      prolong(l, C.u, u, u, uz ? 0 : 1);
       uz = false;
     } else {
       for (int k = 0; k < mu; ++k) {
         cycle(l - 1, C.f, C.u);
-        spmv(V.P, C.u, uz ? nullptr : u, u, uz ? 0 : 1, K_TRANSFER);
+        prolong(l, C.u, u, u, uz ? 0 : 1);
         uz = false;
         if (mu > 1) restrict_residual(l, f, u, uz, C.f);
       }
@@ -976,6 +1000,146 @@ int igb_set_prolongation(igb_ctx* ctx, int level, int n_fine, int n_coarse, long
       }
     V.PT = upload_csr(ctx, n_coarse, n_fine, nnz, tp.data(), ti.data(), tv.data());
     V.has_P = true;
+  });
+}
+
+int igb_set_prolongation_kron(igb_ctx* ctx, int level, int dim, int npatch, const int* nf, const int* nc,
+                              int width, const int* p1_idx, const double* p1_val, const int* fine_free,
+                              const int* fine_owner, const int* coarse_free) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    if (level < 1 || level > ctx->L) throw ArgError("prolongation level must be in 1..L");
+    Level& V = ctx->lev[level];
+    Level& C = ctx->lev[level - 1];
+    if (!V.n || !C.n) throw StateError("set the level matrices before the prolongation");
+    if (V.has_kron) throw StateError("Kronecker prolongation already set");
+    if (dim != 2 && dim != 3) throw ArgError("Kronecker prolongation needs dim 2 or 3");
+    if (npatch < 1) throw ArgError("need at least one patch");
+    if (npatch > KRON_MAXP) return;  // more patches than the parameter tables: CSR transfer stays
+    if (width < 1 || !nf || !nc || !p1_idx || !p1_val || !fine_free || !fine_owner || !coarse_free)
+      throw ArgError("null Kronecker prolongation array");
+    KronArgs& a = V.kron;
+    a = KronArgs{};
+    a.dim = dim;
+    a.npatch = npatch;
+    const int Wd = kron_width(width);  // device ELL width (compiled variants)
+    a.width = Wd;
+    a.n_fine = V.n;
+    a.n_coarse = C.n;
+    std::vector<KronPatch> pt(npatch);
+    std::vector<long long> off_f(npatch + 1, 0), off_c(npatch + 1, 0);
+    long long rows = 0;
+    for (int k = 0; k < npatch; ++k) {
+      long long pf = 1, pc = 1;
+      for (int d = 0; d < 3; ++d) {
+        pt[k].nf[d] = d < dim ? nf[k * dim + d] : 1;
+        pt[k].nc[d] = d < dim ? nc[k * dim + d] : 1;
+        if (pt[k].nf[d] < 1 || pt[k].nc[d] < 1) throw ArgError("empty patch block");
+        pt[k].ell[d] = pt[k].ellT[d] = 0;
+      }
+      for (int d = 0; d < dim; ++d) {
+        pt[k].ell[d] = rows * Wd;
+        rows += pt[k].nf[d];
+        pf *= pt[k].nf[d];
+        pc *= pt[k].nc[d];
+      }
+      off_f[k + 1] = off_f[k] + pf;
+      off_c[k + 1] = off_c[k] + pc;
+    }
+    const long long bf = off_f[npatch], bc = off_c[npatch];
+    a.nblk_f = bf;
+    a.nblk_c = bc;
+    if (Wd < 0) return;  // wider 1-D rows than any compiled variant: the CSR transfer stays
+    std::vector<int> pidx((size_t)rows * Wd, -1);
+    std::vector<double> pval((size_t)rows * Wd, 0.0);
+    // 1-D transposes (ELL rows of widthT, fine index ascending)
+    std::vector<std::vector<std::pair<int, double>>> trows;
+    int wt = 1;
+    for (int k = 0; k < npatch; ++k)
+      for (int d = 0; d < dim; ++d) {
+        std::vector<std::vector<std::pair<int, double>>> t(pt[k].nc[d]);
+        for (int i = 0; i < pt[k].nf[d]; ++i)
+          for (int jj = 0; jj < width; ++jj) {
+            const long long e = (pt[k].ell[d] / Wd + i) * width + jj;  // input rows have `width`
+            const int c = p1_idx[e];
+            if (c < 0) continue;
+            if (c >= pt[k].nc[d]) throw ArgError("1-D prolongation column out of range");
+            t[c].emplace_back(i, p1_val[e]);
+            pidx[(pt[k].ell[d] / Wd + i) * Wd + jj] = c;
+            pval[(pt[k].ell[d] / Wd + i) * Wd + jj] = p1_val[e];
+          }
+        pt[k].ellT[d] = (long long)trows.size();  // rows; scaled by widthT below
+        for (auto& r : t) {
+          wt = std::max(wt, (int)r.size());
+          trows.push_back(std::move(r));
+        }
+      }
+    wt = kron_width_t(wt);
+    if (wt < 0) return;
+    a.widthT = wt;
+    for (int k = 0; k < npatch; ++k)
+      for (int d = 0; d < dim; ++d) pt[k].ellT[d] *= wt;
+    std::vector<int> ti(trows.size() * wt, -1);
+    std::vector<double> tv(trows.size() * wt, 0.0);
+    for (size_t r = 0; r < trows.size(); ++r)
+      for (size_t jj = 0; jj < trows[r].size(); ++jj) {
+        ti[r * wt + jj] = trows[r][jj].first;
+        tv[r * wt + jj] = trows[r][jj].second;
+      }
+    // fine: every free DoF has exactly one owner copy; coarse: root copy + list of the others
+    std::vector<int> fown(bf, -1), seen(V.n, 0);
+    for (long long b = 0; b < bf; ++b) {
+      const int f = fine_free[b];
+      if (f < -1 || f >= V.n) throw ArgError("fine block map out of range");
+      if (f >= 0 && fine_owner[b]) {
+        if (seen[f]++) throw ArgError("fine free DoF with two owner copies");
+        fown[b] = f;
+      }
+    }
+    for (int f = 0; f < V.n; ++f)
+      if (!seen[f]) throw ArgError("fine free DoF without an owner copy");
+    std::vector<int> croot(bc, -1), xptr(C.n + 1, 0), xblk, first(C.n, -1);
+    for (long long b = 0; b < bc; ++b) {
+      const int jj = coarse_free[b];
+      if (jj < -1 || jj >= C.n) throw ArgError("coarse block map out of range");
+      if (jj < 0) continue;
+      if (first[jj] < 0) {
+        first[jj] = (int)b;
+        croot[b] = jj;
+      } else {
+        xptr[jj + 1]++;
+      }
+    }
+    for (int jj = 0; jj < C.n; ++jj) {
+      if (first[jj] < 0) throw ArgError("coarse free DoF without a block copy");
+      xptr[jj + 1] += xptr[jj];
+    }
+    xblk.resize(xptr[C.n]);
+    std::vector<int> pos(xptr.begin(), xptr.end() - 1);
+    for (long long b = 0; b < bc; ++b) {
+      const int jj = coarse_free[b];
+      if (jj >= 0 && first[jj] != (int)b) xblk[pos[jj]++] = (int)b;
+    }
+    for (int k = 0; k < npatch; ++k) a.patch[k] = pt[k];
+    for (int k = 0; k <= npatch; ++k) {
+      a.off_f[k] = off_f[k];
+      a.off_c[k] = off_c[k];
+    }
+    a.pidx = ctx->upload(pidx.data(), pidx.size());
+    a.pval = ctx->upload(pval.data(), pval.size());
+    a.tidx = ctx->upload(ti.data(), ti.size());
+    a.tval = ctx->upload(tv.data(), tv.size());
+    a.fown = ctx->upload(fown.data(), fown.size());
+    a.cfree = ctx->upload(coarse_free, (size_t)bc);
+    a.croot = ctx->upload(croot.data(), croot.size());
+    a.xptr = ctx->upload(xptr.data(), xptr.size());
+    a.xblk = xblk.empty() ? ctx->alloc<int>(1) : ctx->upload(xblk.data(), xblk.size());
+    // measured on B200 (cfg2, cfg5 L=3): the CSR pair is ~3 us per launch faster at these sizes
+    // (transfers are latency-bound; the Kronecker gather chain is one memory latency longer),
+    // so the Kronecker form is opt-in: IGB_TRANSFER=kron
+    const char* te = std::getenv("IGB_TRANSFER");
+    V.has_kron = te && std::string(te) == "kron";
   });
 }
 
@@ -1523,7 +1687,7 @@ int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out) {
           if (level < 1) throw ArgError("restriction needs level >= 1");
           Level& C = ctx->lev[level - 1];
           CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-          ctx->spmv(V.PT, V.f, nullptr, C.r, 0, K_TRANSFER);
+          ctx->restrict_to(level, V.f, C.r);
           CU(cudaMemcpyAsync(out, C.r, sizeof(double) * C.n, cudaMemcpyDeviceToHost, s));
           break;
         }
@@ -1531,7 +1695,7 @@ int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out) {
           if (level < 1) throw ArgError("prolongation needs level >= 1");
           Level& C = ctx->lev[level - 1];
           CU(cudaMemcpyAsync(C.r, in, sizeof(double) * C.n, cudaMemcpyHostToDevice, s));
-          ctx->spmv(V.P, C.r, nullptr, V.r, 0, K_TRANSFER);
+          ctx->prolong(level, C.r, nullptr, V.r, 0);
           CU(cudaMemcpyAsync(out, V.r, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
           break;
         }

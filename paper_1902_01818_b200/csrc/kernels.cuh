@@ -162,6 +162,31 @@ int flow_max_ctas();  // co-resident CTAs of FLOW_NT threads (all variants)
 void flow_set_carveout(int pct);
 void launch_flow_sweep(cudaStream_t s, const FlowArgs& a);
 
+// ---- intergrid transfers as per-patch Kronecker products (transfer.cu) --------------
+struct KronPatch {
+  int nf[3], nc[3];            // block sizes per axis (1 past dim)
+  long long ell[3], ellT[3];   // row-0 offsets of P_{k,a} / P_{k,a}^T in the ELL pools
+};
+constexpr int KRON_MAXP = 16;  // patches per level in the kernel-parameter tables (size: launch cost)
+struct KronArgs {
+  int dim, npatch, width, widthT, n_fine, n_coarse;
+  long long nblk_f, nblk_c;
+  KronPatch patch[KRON_MAXP];                     // per-patch sizes and ELL row offsets
+  long long off_f[KRON_MAXP + 1], off_c[KRON_MAXP + 1];  // block offsets
+  const int* pidx; const double* pval;    // ELL rows (width) of the 1-D matrices, col -1 = pad
+  const int* tidx; const double* tval;    // ELL rows (widthT) of their transposes
+  const int* fown;   // fine block -> free if the copy is the owner (class root), else -1
+  const int* cfree;  // coarse block -> free (-1: Dirichlet)
+  const int* croot;  // coarse block -> free if the copy is the class root, else -1
+  const int* xptr; const int* xblk;  // coarse free DoF -> its non-root block copies
+};
+void kron_set_carveout(int pct);
+int kron_width(int w);    // compiled ELL widths: smallest >= w, -1 if none
+int kron_width_t(int w);
+void launch_kron_prolong(cudaStream_t s, const KronArgs& a, const double* e, const double* z, double* y,
+                         int accumulate);
+void launch_kron_restrict(cudaStream_t s, const KronArgs& a, const double* r, double* y);
+
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
 // y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
 // out[i] = w[perm_c[i]].  Column j updates run in parallel; one barrier per column.

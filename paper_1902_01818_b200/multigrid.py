@@ -195,6 +195,8 @@ class MultigridSolver:
             ctx.set_level_matrix(level, self.A[level])
         for level in range(1, L + 1):
             ctx.set_prolongation(level, self.P[level])
+            if len(self.hier.spaces[level][0]) in (2, 3):
+                ctx.set_prolongation_kron(level, assembly.prolongation_kron(self.hier, level))
         for level in range(1, L + 1):
             smo = self.smoother[level]
             gs = smo if isinstance(smo, sm.GaussSeidel) else getattr(smo, "gs", None)

@@ -270,3 +270,34 @@ def test_flow_engine_matches_oracle(cfg, kw, G):
     _check_history(rep.residuals, histo, "flow vs oracle")
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg2", {"levels": 3}), ("cfg3", {"levels": 2}), ("cfg5", {"levels": 2}),
+                                    ("cfg4", {"p": 4, "levels": 2})])
+def test_kronecker_transfers_match_P(cfg, kw):
+    """IGB_TRANSFER=kron: restriction / prolongation as per-patch Kronecker products of the 1-D
+    two-scale matrices (transfer.cu) against the reference-form P, and the PCG solve on them."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup(cfg, **kw)
+    os.environ["IGB_TRANSFER"] = "kron"
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_TRANSFER"]
+    rng = np.random.default_rng(31)
+    for level in range(1, solver.finest + 1):
+        n, nc = solver.A[level].shape[0], solver.A[level - 1].shape[0]
+        x, xc = rng.standard_normal(n), rng.standard_normal(nc)
+        r1 = solver.ctx.op("restrict", level, x, nc)
+        assert rel(r1, solver.P[level].T @ x) <= 1e-13
+        assert np.array_equal(solver.ctx.op("restrict", level, x, nc), r1)  # fixed summation order
+        assert rel(solver.ctx.op("prolong", level, xc, n), solver.P[level] @ xc) <= 1e-13
+    orc = OracleSolver(setup.setup_bundle())
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, "kron transfers vs oracle")
+    assert rel(rep.x, xo) <= 1e-10
+    solver.close()

@@ -110,3 +110,20 @@ def test_matrices_equal_reference_directly():
         assert (d.max() if d.nnz else 0.0) <= 1e-13 * abs(rs.A[l]).max()
     for l in range(1, 3):
         assert abs(rs.P[l] - ms.P[l]).nnz == 0
+
+
+@pytest.mark.parametrize("name,kw", [("cfg1", {}), ("cfg2", {"levels": 3}), ("cfg3", {"levels": 2}),
+                                     ("cfg4", {"p": 4, "levels": 2}), ("cfg5", {"levels": 1})])
+def test_kronecker_transfer_description_reproduces_P(name, kw):
+    """The per-patch Kronecker description the device transfer uses (1-D two-scale matrices,
+    block maps, owner copies) reproduces the reference-form P and P^T to rounding."""
+    from paper_1902_01818_b200 import assembly, configs
+    pr = configs.build(name, **kw)
+    rng = np.random.default_rng(4)
+    for level in range(1, pr.hier.L + 1):
+        P = assembly.prolongation(pr.hier, level)
+        kd = assembly.prolongation_kron(pr.hier, level)
+        assert kd["fine_owner"][kd["fine_free"] >= 0].sum() == P.shape[0]
+        x, y = rng.standard_normal(P.shape[1]), rng.standard_normal(P.shape[0])
+        assert np.abs(assembly.kron_apply(kd, x) - P @ x).max() <= 1e-14 * np.abs(P @ x).max()
+        assert np.abs(assembly.kron_apply(kd, y, True) - P.T @ y).max() <= 1e-14 * np.abs(P.T @ y).max()

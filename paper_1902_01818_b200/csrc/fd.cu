@@ -24,19 +24,22 @@ namespace {
 
 constexpr int FDC_KC = 16;  // gathered-operand rows per chunk
 
-template <int RB>
+// NM = largest interior side of the variant, NT = threads (one column each, NT >= NM).
+// WHOLE: products 2-4 copy their right operand whole into shared memory (NM = 160); else every
+// product streams it in chunks (NM = 264: a 264^2 operand does not fit).
+template <int RB, int NM, bool WHOLE>
 size_t fd_smem(int kmax) {
-  // right-operand buffer: whole operand (kmax rows) or the two gather chunks, whichever is larger
-  return 8 * (2 * (size_t)FDC_NMAX * RB + (size_t)(kmax > 2 * FDC_KC ? kmax : 2 * FDC_KC) * FDC_NMAX);
+  const size_t rs = WHOLE ? (size_t)(kmax > 2 * FDC_KC ? kmax : 2 * FDC_KC) * NM : (size_t)2 * FDC_KC * NM;
+  return 8 * (2 * (size_t)NM * RB + rs);
 }
 
 // Gathered right operand (R = r[idx], step 1): 16-row chunks, each thread loading its column
 // of the next chunk into registers while the current one is multiplied (plain loads; 8-byte
 // cp.async copies of a gather measured slower).  rch: two [FDC_KC][FDC_NMAX] chunks.
-template <int RB, class Load>
+template <int RB, int NM, class Load>
 __device__ __forceinline__ void fdc_gemm_chunked(double (&acc)[RB], const double (*L)[RB], int K, int j,
                                                  double* rch_base, Load ld) {
-  double (*rch)[FDC_KC][FDC_NMAX] = reinterpret_cast<double (*)[FDC_KC][FDC_NMAX]>(rch_base);
+  double (*rch)[FDC_KC][NM] = reinterpret_cast<double (*)[FDC_KC][NM]>(rch_base);
 #pragma unroll
   for (int i = 0; i < RB; ++i) acc[i] = 0.0;
   double pre[FDC_KC];
@@ -44,7 +47,7 @@ __device__ __forceinline__ void fdc_gemm_chunked(double (&acc)[RB], const double
   for (int k = 0; k < FDC_KC; ++k) pre[k] = ld(min(k, K - 1));  // clamped rows are never consumed
   const int nch = (K + FDC_KC - 1) / FDC_KC;
   for (int q = 0; q < nch; ++q) {
-    double (*buf)[FDC_NMAX] = rch[q & 1];
+    double (*buf)[NM] = rch[q & 1];
 #pragma unroll
     for (int k = 0; k < FDC_KC; ++k) buf[k][j] = pre[k];
     __syncthreads();
@@ -73,12 +76,12 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
 // shared buffer Rs ([m][FDC_NMAX]) at once -- every thread issues cp.async for its column of
 // all K rows (8-byte copies, so gathered operands work too) -- one memory latency per product,
 // then the multiply runs from shared memory.  The caller synchronises before Rs is reused.
-template <int RB, class Addr>
+template <int RB, int NM, class Addr>
 __device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB], int K, int j, bool active,
                                          double* Rs, Addr addr) {
   if (active) {
 #pragma unroll 4
-    for (int m = 0; m < K; ++m) cp_async8(Rs + m * FDC_NMAX + j, addr(m));
+    for (int m = 0; m < K; ++m) cp_async8(Rs + m * NM + j, addr(m));
   }
   asm volatile("cp.async.commit_group;" ::: "memory");
   asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -88,7 +91,7 @@ __device__ __forceinline__ void fdc_gemm(double (&acc)[RB], const double (*L)[RB
   const double* x = Rs + j;
 #pragma unroll 8
   for (int m = 0; m < K; ++m) {
-    const double xm = x[m * FDC_NMAX];
+    const double xm = x[m * NM];
     const double* l = L[m];
 #pragma unroll
     for (int i = 0; i < RB; ++i) acc[i] = fma(l[i], xm, acc[i]);
@@ -120,45 +123,50 @@ __device__ __forceinline__ FdCtx fd_locate(const FdBatch& bt) {
 
 // left-operand fill: lop[m][i] = T0[m][r0+i] (cols) or T0[r0+i][m] (rows); every load of a
 // thread is issued before its stores (one round trip)
-template <int RB>
+template <int RB, int NM, int NT>
 __device__ __forceinline__ void fd_fill(double (*lop)[RB], const FdCtx& c, bool rows) {
-  constexpr int FILL = (FDC_NMAX * RB + FDC_NT - 1) / FDC_NT;
+  constexpr int FILL = (NM * RB + NT - 1) / NT;
   double v[FILL];
 #pragma unroll
   for (int q = 0; q < FILL; ++q) {
-    const int e = c.j + q * FDC_NT, m = e / RB, i = e - m * RB;
+    const int e = c.j + q * NT, m = e / RB, i = e - m * RB;
     const int mm = min(m, c.n0 - 1), ii = min(i, max(c.nr - 1, 0));
     v[q] = __ldg(c.it.T0 + (rows ? (size_t)(c.r0 + ii) * c.n0 + mm : (size_t)mm * c.n0 + c.r0 + ii));
   }
 #pragma unroll
   for (int q = 0; q < FILL; ++q) {
-    const int e = c.j + q * FDC_NT, m = e / RB, i = e - m * RB;
+    const int e = c.j + q * NT, m = e / RB, i = e - m * RB;
     if (m < c.n0) lop[m][i] = i < c.nr ? v[q] : 0.0;
   }
 }
 
-template <int RB>
-__global__ void __launch_bounds__(FDC_NT, 2) fd_front_kernel(const __grid_constant__ FdBatch bt, const double* r) {
+template <int RB, int NM, int NT, bool WHOLE>
+__global__ void __launch_bounds__(NT, 2) fd_front_kernel(const __grid_constant__ FdBatch bt, const double* r) {
   pdl_begin();
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
-  double (*outT)[RB] = lop + FDC_NMAX;
-  double* Rs = fdc_smem + 2 * FDC_NMAX * RB;  // [kmax][FDC_NMAX] right operand
+  double (*outT)[RB] = lop + NM;
+  double* Rs = fdc_smem + 2 * NM * RB;  // right operand (whole [kmax][NM], or two chunks)
   const FdCtx c = fd_locate(bt);
   const int n1 = c.n1, jj = c.jj;
   double acc[RB];
   // 1: B = T0^T R
-  fd_fill<RB>(lop, c, false);
+  fd_fill<RB, NM, NT>(lop, c, false);
   __syncthreads();
   if (c.j == 0)  // step 2's operand: into L2 while step 1 runs
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(c.it.T1), "r"((unsigned)(8 * n1 * n1) & ~15u)
                  : "memory");
-  fdc_gemm_chunked<RB>(acc, lop, c.n0, c.j, Rs, [&](int m) { return r[__ldg(c.it.idx + (size_t)m * n1 + jj)]; });
+  fdc_gemm_chunked<RB, NM>(acc, lop, c.n0, c.j, Rs, [&](int m) { return r[__ldg(c.it.idx + (size_t)m * n1 + jj)]; });
+  if (c.j < NM) {
 #pragma unroll
-  for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
+    for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
+  }
   __syncthreads();
   // 2: A = (B T1) ./ D    left outT[m][i] = B[i][m]
-  fdc_gemm<RB>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)m * n1 + jj; });
+  if (WHOLE)
+    fdc_gemm<RB, NM>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)m * n1 + jj; });
+  else
+    fdc_gemm_chunked<RB, NM>(acc, outT, n1, c.j, Rs, [&](int m) { return __ldg(c.it.T1 + (size_t)m * n1 + jj); });
   if (c.active) {
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -187,9 +195,9 @@ __device__ void fd_piece_rows(const PieceRowBlock& b, const double* r, double* u
   }
 }
 
-template <int RB>
-__global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, const double* r,
-                                                         double* u, double alpha, int accumulate) {
+template <int RB, int NM, int NT, bool WHOLE>
+__global__ void __launch_bounds__(NT, 2) fd_back_kernel(const __grid_constant__ FdBatch bt, const double* r,
+                                                        double* u, double alpha, int accumulate) {
   pdl_begin();
   if ((int)blockIdx.x >= bt.cta0[bt.nitems]) {
     fd_piece_rows(bt.pieces[blockIdx.x - bt.cta0[bt.nitems]], r, u, alpha, accumulate);
@@ -197,23 +205,31 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constan
   }
   extern __shared__ __align__(16) double fdc_smem[];
   double (*lop)[RB] = reinterpret_cast<double (*)[RB]>(fdc_smem);
-  double (*outT)[RB] = lop + FDC_NMAX;
-  double* Rs = fdc_smem + 2 * FDC_NMAX * RB;  // [kmax][FDC_NMAX] right operand
+  double (*outT)[RB] = lop + NM;
+  double* Rs = fdc_smem + 2 * NM * RB;
   const FdCtx c = fd_locate(bt);
   const int n1 = c.n1, jj = c.jj;
   double acc[RB];
   // 3: B' = T0 A
-  fd_fill<RB>(lop, c, true);
+  fd_fill<RB, NM, NT>(lop, c, true);
   int gi[RB];  // epilogue targets, fetched two products ahead
 #pragma unroll
   for (int i = 0; i < RB; ++i) gi[i] = __ldg(c.it.idx + (size_t)(c.r0 + min(i, max(c.nr - 1, 0))) * n1 + jj);
   __syncthreads();
-  fdc_gemm<RB>(acc, lop, c.n0, c.j, c.active, Rs, [&](int m) { return c.it.scratch + (size_t)m * n1 + jj; });
+  if (WHOLE)
+    fdc_gemm<RB, NM>(acc, lop, c.n0, c.j, c.active, Rs, [&](int m) { return c.it.scratch + (size_t)m * n1 + jj; });
+  else
+    fdc_gemm_chunked<RB, NM>(acc, lop, c.n0, c.j, Rs, [&](int m) { return c.it.scratch[(size_t)m * n1 + jj]; });
+  if (c.j < NM) {
 #pragma unroll
-  for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
+    for (int i = 0; i < RB; ++i) outT[c.j][i] = acc[i];
+  }
   __syncthreads();
   // 4: X = B' T1^T       right T1[j][m]
-  fdc_gemm<RB>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)jj * n1 + m; });
+  if (WHOLE)
+    fdc_gemm<RB, NM>(acc, outT, n1, c.j, c.active, Rs, [&](int m) { return c.it.T1 + (size_t)jj * n1 + m; });
+  else
+    fdc_gemm_chunked<RB, NM>(acc, outT, n1, c.j, Rs, [&](int m) { return __ldg(c.it.T1 + (size_t)jj * n1 + m); });
   if (c.active) {
 #pragma unroll
     for (int i = 0; i < RB; ++i)
@@ -224,18 +240,21 @@ __global__ void __launch_bounds__(FDC_NT, 2) fd_back_kernel(const __grid_constan
   }
 }
 
-template <int RB>
+template <int RB, int NM, int NT, bool WHOLE>
 void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(fd_front_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>(FDC_NMAX));
-    cudaFuncSetAttribute(fd_back_kernel<RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fd_smem<RB>(FDC_NMAX));
+    cudaFuncSetAttribute(fd_front_kernel<RB, NM, NT, WHOLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fd_smem<RB, NM, WHOLE>(NM));
+    cudaFuncSetAttribute(fd_back_kernel<RB, NM, NT, WHOLE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)fd_smem<RB, NM, WHOLE>(NM));
     attr = true;
   }
   const int grid = bt.cta0[bt.nitems];
-  const size_t smem = fd_smem<RB>(bt.kmax);
-  launch_k(fd_front_kernel<RB>, dim3(grid), dim3(FDC_NT), smem, s, bt, r);
-  launch_k(fd_back_kernel<RB>, dim3(grid + bt.npieces), dim3(FDC_NT), smem, s, bt, r, u, alpha, accumulate);
+  const size_t smem = fd_smem<RB, NM, WHOLE>(bt.kmax);
+  launch_k(fd_front_kernel<RB, NM, NT, WHOLE>, dim3(grid), dim3(NT), smem, s, bt, r);
+  launch_k(fd_back_kernel<RB, NM, NT, WHOLE>, dim3(grid + bt.npieces), dim3(NT), smem, s, bt, r, u, alpha,
+           accumulate);
 }
 
 }  // namespace
@@ -248,18 +267,31 @@ int fd_rows_per_cta(int total_rows) {
 
 void launch_fd_batch(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate) {
   if (bt.nitems <= 0) return;
+  if (bt.large) {
+    switch (bt.rb) {
+      case 2: launch_rb<2, FDL_NMAX, FDL_NT, false>(s, bt, r, u, alpha, accumulate); break;
+      case 4: launch_rb<4, FDL_NMAX, FDL_NT, false>(s, bt, r, u, alpha, accumulate); break;
+      default: launch_rb<8, FDL_NMAX, FDL_NT, false>(s, bt, r, u, alpha, accumulate); break;
+    }
+    return;
+  }
   switch (bt.rb) {
-    case 2: launch_rb<2>(s, bt, r, u, alpha, accumulate); break;
-    case 4: launch_rb<4>(s, bt, r, u, alpha, accumulate); break;
-    default: launch_rb<8>(s, bt, r, u, alpha, accumulate); break;
+    case 2: launch_rb<2, FDC_NMAX, FDC_NT, true>(s, bt, r, u, alpha, accumulate); break;
+    case 4: launch_rb<4, FDC_NMAX, FDC_NT, true>(s, bt, r, u, alpha, accumulate); break;
+    default: launch_rb<8, FDC_NMAX, FDC_NT, true>(s, bt, r, u, alpha, accumulate); break;
   }
 }
 
 void set_carveout_panel(int pct);  // panel.cu
 
 void set_carveout_panel_fd(int pct) {
-  for (const void* f : {(const void*)fd_front_kernel<2>, (const void*)fd_back_kernel<2>, (const void*)fd_front_kernel<4>,
-                        (const void*)fd_back_kernel<4>, (const void*)fd_front_kernel<8>, (const void*)fd_back_kernel<8>})
+  for (const void* f :
+       {(const void*)fd_front_kernel<2, FDC_NMAX, FDC_NT, true>, (const void*)fd_back_kernel<2, FDC_NMAX, FDC_NT, true>,
+        (const void*)fd_front_kernel<4, FDC_NMAX, FDC_NT, true>, (const void*)fd_back_kernel<4, FDC_NMAX, FDC_NT, true>,
+        (const void*)fd_front_kernel<8, FDC_NMAX, FDC_NT, true>, (const void*)fd_back_kernel<8, FDC_NMAX, FDC_NT, true>,
+        (const void*)fd_front_kernel<2, FDL_NMAX, FDL_NT, false>, (const void*)fd_back_kernel<2, FDL_NMAX, FDL_NT, false>,
+        (const void*)fd_front_kernel<4, FDL_NMAX, FDL_NT, false>, (const void*)fd_back_kernel<4, FDL_NMAX, FDL_NT, false>,
+        (const void*)fd_front_kernel<8, FDL_NMAX, FDL_NT, false>, (const void*)fd_back_kernel<8, FDL_NMAX, FDL_NT, false>})
     cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaGetLastError();
   set_carveout_panel(pct);

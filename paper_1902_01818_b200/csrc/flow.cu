@@ -121,6 +121,8 @@ __global__ void __launch_bounds__(FLOW_NT) flow_sweep_kernel(FlowArgs a) {
       }
     }
     if (a.crit) __syncwarp();
+    long long cc0 = 0;
+    if (a.trace && gl == 0) cc0 = clock64();
     double acc = 0.0;
     for (int base = s; base < e; base += G * K) {
       int c[K];
@@ -168,12 +170,13 @@ __global__ void __launch_bounds__(FLOW_NT) flow_sweep_kernel(FlowArgs a) {
       st_relaxed(xg_set + row, xv);
       xg_clr[row] = __longlong_as_double((long long)FLOW_PENDING);
       a.u[row] = a.accumulate ? uold + xv : xv;
-      if (a.trace) {  // [start time, ready - start cycles, stored - ready cycles, stored time]
+      if (a.trace) {  // [start time, crit seen - start, ready - crit seen, stored - ready (cycles), stored time]
         const long long c2 = clock64();
-        a.trace[4 * q] = t0;
-        a.trace[4 * q + 1] = c1 - c0;
-        a.trace[4 * q + 2] = c2 - c1;
-        a.trace[4 * q + 3] = gtime();
+        a.trace[5 * q] = t0;
+        a.trace[5 * q + 1] = cc0 - c0;
+        a.trace[5 * q + 2] = c1 - cc0;
+        a.trace[5 * q + 3] = c2 - c1;
+        a.trace[5 * q + 4] = gtime();
       }
     }
   }

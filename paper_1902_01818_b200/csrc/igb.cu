@@ -382,16 +382,16 @@ struct igb_ctx {
         const char* tr = std::getenv("IGB_FLOW_TRACE");
         long long* dtr = nullptr;
         if (tr) {
-          CU(cudaMalloc(&dtr, 4 * sizeof(long long) * a.nq));
-          CU(cudaMemsetAsync(dtr, 0, 4 * sizeof(long long) * a.nq, stream));
+          CU(cudaMalloc(&dtr, 5 * sizeof(long long) * a.nq));
+          CU(cudaMemsetAsync(dtr, 0, 5 * sizeof(long long) * a.nq, stream));
           a.trace = dtr;
         }
         CU(cudaEventRecord(e0, stream));
         launch_flow_sweep(stream, a);
         CU(cudaEventRecord(e1, stream));
         CU(cudaEventSynchronize(e1));
-        if (tr) {  // binary dump: int nq, int[nq] row, int[nq] level, int64[4 nq] trace
-          std::vector<long long> ht(4 * (size_t)a.nq);
+        if (tr) {  // binary dump: int nq, int[nq] row, int[nq] level, int64[5 nq] trace
+          std::vector<long long> ht(5 * (size_t)a.nq);
           CU(cudaMemcpy(ht.data(), dtr, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
           cudaFree(dtr);
           char path[512];
@@ -751,32 +751,51 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
   if (V.interiors.empty()) return;
   int dim = V.interiors[0].dim;
   // 2-D interiors up to FDC_NMAX: one fused cluster each; the rest: batched GEMM steps
-  std::vector<FdCluster> clu;
+  std::vector<FdCluster> clu, clu_large;
   std::vector<InteriorStage> big;
+  static const bool large_ok = !(std::getenv("IGB_FD_LARGE") && std::atoi(std::getenv("IGB_FD_LARGE")) == 0);
   const bool fuse = !(std::getenv("IGB_FD_FUSE") && std::string(std::getenv("IGB_FD_FUSE")) == "0");
   for (auto& it : V.interiors) {
     if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
     if (fuse && dim == 2 && it.n[0] <= FDC_NMAX && it.n[1] <= FDC_NMAX) {
       clu.push_back(FdCluster{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]});
+    } else if (fuse && large_ok && dim == 2 && it.n[0] <= FDL_NMAX && it.n[1] <= FDL_NMAX) {
+      clu_large.push_back(FdCluster{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]});
     } else {
       big.push_back(it);
     }
   }
-  if (!clu.empty()) {
+  {
+    // the chunked variant re-streams the right operand from L2 per CTA: measured better than the
+    // batched GEMM for a few large interiors (cfg3: one 258^2, 22.2 vs 24.3 ms per solve), worse
+    // for many (cfg4: sixteen 256^2, 27.4 vs 25.2 ms)
+    long long rows = 0;
+    for (auto& f : clu_large) rows += f.n0;
+    if (rows > 1024) {
+      for (auto& it : V.interiors)
+        if (it.dim == 2 && std::max(it.n[0], it.n[1]) > FDC_NMAX && std::max(it.n[0], it.n[1]) <= FDL_NMAX)
+          big.push_back(it);
+      clu_large.clear();
+    }
+  }
+  for (int large = 0; large < 2; ++large) {
+    std::vector<FdCluster>& cl = large ? clu_large : clu;
+    if (cl.empty()) continue;
     size_t tot = 0;
-    for (auto& f : clu) tot += (size_t)f.n0 * f.n1;
+    for (auto& f : cl) tot += (size_t)f.n0 * f.n1;
     double* scratch = ctx->alloc<double>(tot);
-    for (auto& f : clu) {
+    for (auto& f : cl) {
       f.scratch = scratch;
       scratch += (size_t)f.n0 * f.n1;
     }
-    for (size_t b0 = 0; b0 < clu.size(); b0 += FD_BATCH_MAX) {
+    for (size_t b0 = 0; b0 < cl.size(); b0 += FD_BATCH_MAX) {
       FdBatch bt{};
-      bt.nitems = (int)std::min<size_t>(FD_BATCH_MAX, clu.size() - b0);
+      bt.large = large;
+      bt.nitems = (int)std::min<size_t>(FD_BATCH_MAX, cl.size() - b0);
       int rows = 0;
       double bytes = 0;
       for (int i = 0; i < bt.nitems; ++i) {
-        bt.items[i] = clu[b0 + i];
+        bt.items[i] = cl[b0 + i];
         rows += bt.items[i].n0;
         const double n0 = bt.items[i].n0, n1 = bt.items[i].n1;
         // T0 and T1 read twice, R gathered, D, A written + read, X scattered

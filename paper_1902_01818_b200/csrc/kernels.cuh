@@ -247,6 +247,8 @@ struct PieceRowBlock {
 // n0, n1 <= FDC_NMAX; scratch: n0 * n1 doubles per interior (the middle intermediate).
 constexpr int FDC_NMAX = 160;
 constexpr int FDC_NT = 160;
+constexpr int FDL_NMAX = 264;  // large variant: right operands streamed in chunks
+constexpr int FDL_NT = 264;   // one column per thread (8.25 warps)
 constexpr int FD_BATCH_MAX = 16;
 struct FdCluster {
   const double* T0;
@@ -262,6 +264,7 @@ struct FdBatch {
   int nitems;
   int rb;                      // rows per CTA: 2, 4 or 8
   int kmax;                    // largest n0 / n1 of the batch (shared-memory buffer rows)
+  int large;                   // 1: the FDL_NMAX variant (chunked right operands)
   const PieceRowBlock* pieces; // interface-piece rows (<= 5 per block) done by extra CTAs of
   int npieces;                 // the back kernel (disjoint u entries), or none
 };

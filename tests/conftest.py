@@ -32,6 +32,9 @@ SMALL_CASES = [
     ("cfg4_p2_L3", "cfg4", {"p": 2, "levels": 3}),
     ("cfg4_p4_L3", "cfg4", {"p": 4, "levels": 3}),
     ("cfg5_L1", "cfg5", {"levels": 1}),
+    ("cfg5_L2", "cfg5", {"levels": 2}),
+    ("cfg4_p6_L3", "cfg4", {"p": 6, "levels": 3}),
+    ("cfg4_p8_L3", "cfg4", {"p": 8, "levels": 3}),
 ]
 
 _setup_cache = {}

@@ -97,6 +97,11 @@ CASES = {
     "cfg4_p4_L3": (ref_cfg4, {"p": 4, "levels": 3}, "cfg4", {"p": 4, "levels": 3}),
     "cfg5_L1": (ref_cfg5, {"levels": 1}, "cfg5", {"levels": 1}),
     "cfg4_p2": (ref_cfg4, {"p": 2}, "cfg4", {"p": 2}),
+    "cfg5_L2": (ref_cfg5, {"levels": 2}, "cfg5", {"levels": 2}),
+    "cfg4_p8_L3": (ref_cfg4, {"p": 8, "levels": 3}, "cfg4", {"p": 8, "levels": 3}),
+    "cfg4_p6_L3": (ref_cfg4, {"p": 6, "levels": 3}, "cfg4", {"p": 6, "levels": 3}),
+    "cfg5_L3": (ref_cfg5, {"levels": 3}, "cfg5", {"levels": 3}),
+    "cfg4_p4": (ref_cfg4, {"p": 4}, "cfg4", {"p": 4}),
 }
 
 
@@ -155,6 +160,6 @@ def make(name):
 
 
 if __name__ == "__main__":
-    names = sys.argv[1:] or [n for n in CASES if n != "cfg4_p2"]
+    names = sys.argv[1:] or [n for n in CASES if n not in ("cfg4_p2", "cfg5_L3", "cfg4_p4")]
     for n in names:
         make(n)

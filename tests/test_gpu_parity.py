@@ -147,20 +147,25 @@ def test_bad_arguments_are_errors():
 
 
 @pytest.mark.slow
-def test_cfg4_p2_full_size_matches_reference_golden():
-    """cfg4 p=2 at full size (N = 1,054,729; 16 distorted patches; 7 levels).
-
-    Reference golden (tools/make_golden.py, igamg run here): 5 iterations, history, and a strided
-    sample of x.  The device GS here runs as a thread-block cluster (levels of ~256 rows).
-    """
-    g = load_golden("cfg4_p2")
-    pr, setup, f, solver, orc = device_solver("cfg4", p=2)
-    assert np.abs(f[:: int(g["x_sample_step"])] - g["f_sample"]).max() <= 1e-13 * np.abs(g["f_sample"]).max()
+@pytest.mark.parametrize("golden,cfg,kw", [("cfg4_p2", "cfg4", {"p": 2}), ("cfg4_p4", "cfg4", {"p": 4}),
+                                            ("cfg5_L3", "cfg5", {"levels": 3})])
+def test_large_configs_match_reference_golden(golden, cfg, kw):
+    """Large configurations against the reference run here (tools/make_golden.py): cfg4 at full size
+    (p = 2: N = 1,054,729, 26M nnz; p = 4: N = 1,071,225, 86M nnz; 16 distorted patches, 7 levels) and
+    cfg5 at L = 3 (3-D, N = 300,763, 92M nnz; flow sweeps on every level).  Iteration count, the
+    residual history and a strided sample of x (and of f, pinning the host setup)."""
+    g = load_golden(golden)
+    from paper_1902_01818_b200 import multigrid
+    pr, setup, f = get_setup(cfg, **kw)
+    step = int(g["x_sample_step"])
+    assert np.abs(f[::step] - g["f_sample"]).max() <= 1e-13 * np.abs(g["f_sample"]).max()
+    solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
     rep = solver.solve_pcg(f, check_spd=False)
     assert rep.iterations == int(g["its"])
-    _check_history(rep.residuals, g["hist"], "cfg4 p=2 vs reference golden")
-    xs = rep.x[:: int(g["x_sample_step"])]
+    _check_history(rep.residuals, g["hist"], f"{golden} vs reference golden")
+    xs = rep.x[::step]
     assert np.linalg.norm(xs - g["x_sample"]) <= 1e-10 * np.linalg.norm(g["x_sample"])
+    solver.close()
 
 
 def test_gs_cluster_path_matches_oracle():

@@ -28,6 +28,8 @@ METRICS = [
 
 
 def last_json(path):
+    if not os.path.exists(path):
+        return None
     with open(path) as fh:
         for line in reversed(fh.read().strip().splitlines()):
             if line.startswith("{"):

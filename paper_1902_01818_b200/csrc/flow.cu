@@ -29,6 +29,7 @@
 namespace igb {
 namespace {
 
+constexpr int FLOW_MINB = 2;  // resident CTAs per SM the register budget is sized for (3: spills, measured 1.5x slower)
 constexpr unsigned long long FLOW_PENDING = 0x7FF4DEADBEEF5678ULL;
 
 __device__ __forceinline__ double ld_relaxed(const double* p) {
@@ -72,7 +73,7 @@ __device__ __noinline__ void flow_stuck(int col, int row) {
 // and the right-hand side / inverse diagonal loads are pinned at the top of the row (volatile
 // asm: the compiler may not sink them to their use after the poll loop).
 template <int G, int K>
-__global__ void __launch_bounds__(FLOW_NT) flow_sweep_kernel(FlowArgs a) {
+__global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs a) {
   pdl_begin();
   constexpr int RPW = 32 / G;
   const int lane = threadIdx.x & 31, sub = lane / G, gl = lane % G;

@@ -77,6 +77,7 @@ __device__ void finish_reduction(double blocksum, double* partials, unsigned* co
   if (!last) return;
   __threadfence();
   double v = 0.0;
+#pragma unroll 8
   for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) v += __ldcg(&partials[i]);
   v = block_sum(v, red2);
   if (threadIdx.x == 0) {
@@ -88,27 +89,30 @@ __device__ void finish_reduction(double blocksum, double* partials, unsigned* co
 // ---------------------------------------------------------------------------
 // CSR SpMV
 // Row dot product for one lane of a G-lane row group: entries k = b + lane, b + lane + G, ...
-// summed in that order (one accumulator), loads issued four entries ahead for memory-level
-// parallelism on long rows (3-D, high degree).
+// summed in that order (one accumulator).  Loads go out in predicated batches of U entries per
+// lane (all column / value loads, then all gathers): a 3-D row (343 entries, G = 32, U = 12) costs
+// one memory round trip pair instead of one per four entries (ncu: the long-row SpMV was
+// long-scoreboard bound at 43% of DRAM peak with 4 entries in flight).
 template <int G>
 __device__ __forceinline__ double row_dot(int b, int e, int lane, const int* __restrict__ col,
                                           const double* __restrict__ val, const double* __restrict__ x) {
+  constexpr int U = G >= 16 ? 12 : 4;
   double s = 0.0;
-  int k = b + lane;
-  for (; k + 3 * G < e; k += 4 * G) {
-    int c[4];
-    double v[4], xv[4];
+  for (int k = b + lane; k < e; k += U * G) {
+    int c[U];
+    double v[U], xv[U];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      c[j] = __ldg(&col[k + j * G]);
-      v[j] = __ldg(&val[k + j * G]);
+    for (int j = 0; j < U; ++j) {
+      const bool in = k + j * G < e;
+      c[j] = in ? __ldg(&col[k + j * G]) : -1;
+      v[j] = in ? __ldg(&val[k + j * G]) : 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xv[j] = __ldg(&x[c[j]]);
+    for (int j = 0; j < U; ++j) xv[j] = c[j] >= 0 ? __ldg(&x[c[j]]) : 0.0;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s = fma(v[j], xv[j], s);
+    for (int j = 0; j < U; ++j)
+      if (c[j] >= 0) s = fma(v[j], xv[j], s);
   }
-  for (; k < e; k += G) s = fma(__ldg(&val[k]), __ldg(&x[__ldg(&col[k])]), s);
   return s;
 }
 
@@ -795,6 +799,8 @@ void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, cons
                      CgScalars* sc, double* hist) {
   const int bs = 256;
   long long g = ((long long)n * group + bs - 1) / bs;  // one row group per thread group
+  // capped (measured on cfg5 L=3: 2048..16384 blocks within 5%; 37596 = one row group per thread
+  // group 20% slower -- every block ends with an atomic on one counter)
   const int grid = (int)(g < 1 ? 1 : (g > REDUCTION_MAX_BLOCKS ? REDUCTION_MAX_BLOCKS : g));
   switch (group) {
     case 4: launch_k(spmv_dot_kernel<4>, dim3(grid), dim3(bs), 0, s, n, ptr, col, val, d, q, partials, counter, sc, hist); break;

@@ -282,7 +282,7 @@ struct CgScalars {
 };
 enum FinalizeKind { FIN_NORMB = 0, FIN_RZ0 = 1, FIN_ALPHA = 2, FIN_REL = 3, FIN_BETA = 4 };
 
-constexpr int REDUCTION_MAX_BLOCKS = 16384;  // size of the partials buffer
+constexpr int REDUCTION_MAX_BLOCKS = 16384;  // size of the partials buffer (grid-stride beyond)
 int reduction_grid(int n);
 // q = A d ; then partial d.q -> alpha = rz / (d.q)
 void launch_spmv_dot(cudaStream_t s, int n, const int* ptr, const int* col, const double* val,

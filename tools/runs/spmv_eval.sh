@@ -1,5 +1,6 @@
-timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -k "operators or pcg" 2>&1 | tail -2
+timeout 1200 python -m pytest tests/test_gpu_parity.py -x -q -k "operators or pcg_matches" 2>&1 | tail -2
 timeout 600 python bench.py --config cfg5 --levels 3 --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), {k: (round(v['ms_per_step'],3), round(v['GBps'])) for k, v in d['roofline']['classes'].items()})"
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu-baseline 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(round(d['ms_per_step'],3), {k: (round(v['ms_per_step'],3), round(v['GBps'])) for k, v in d['roofline']['classes'].items()})"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:spmv -c 400 --csv python bench.py --config cfg5 --levels 3 --steps 1 --warmup 3 --no-cpu-baseline 2>/dev/null | grep -v "^==" > gpurun_out/spmv_cfg5.csv
 python - <<'PY'
 import csv, collections

@@ -127,6 +127,7 @@ struct Level {
   bool has_gs = false;
   bool has_U = false;
   DevCsr U;  // strict upper triangle of A: residual after a forward sweep from zero is -U c
+  DevCsr Lo; // strict lower triangle: a backward step from u solves triu(A) u' = f - Lo u
   Sched fwd, bwd;
   long long tri_nnz_lower = 0, tri_nnz_upper = 0;
   bool has_scms = false;
@@ -533,11 +534,24 @@ struct igb_ctx {
     else gs(l, kind == 'B', res, u, u_zero);
     u_zero = false;
   }
+  // Gauss-Seidel step from a nonzero u without the full residual: u' = u + T^-1 (f - A u) solves
+  // T u' = f - (A - T) u, T = tril(A) (fwd) or triu(A) (bwd) -- the other strict triangle is
+  // half the matrix traffic of f - A u (same iterate up to rounding)
+  void gs_step(int l, bool upper, const double* f, double* u, bool& u_zero) {
+    Level& V = lev[l];
+    if (u_zero || !V.has_U) {
+      smooth_step(l, upper ? 'B' : 'G', f, u, u_zero);
+      return;
+    }
+    spmv(upper ? V.Lo : V.U, u, f, V.r, -1, K_SPMV);
+    gs(l, upper, V.r, u, true);
+    u_zero = false;
+  }
 
   void pre_smooth(int l, const double* f, double* u, bool& uz) {
     const int st = steps[l];
     if (smoother == IGB_SMOOTHER_GS) {
-      for (int i = 0; i < st; ++i) smooth_step(l, 'G', f, u, uz);
+      for (int i = 0; i < st; ++i) gs_step(l, false, f, u, uz);
     } else if (smoother == IGB_SMOOTHER_SCMS) {
       for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
     } else {
@@ -558,12 +572,12 @@ struct igb_ctx {
   void post_smooth(int l, const double* f, double* u, bool& uz) {
     const int st = steps[l];
     if (smoother == IGB_SMOOTHER_GS) {
-      for (int i = 0; i < st; ++i) smooth_step(l, 'B', f, u, uz);
+      for (int i = 0; i < st; ++i) gs_step(l, true, f, u, uz);
     } else if (smoother == IGB_SMOOTHER_SCMS) {
       for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
     } else {
       for (int i = 0; i < st; ++i) smooth_step(l, 'S', f, u, uz);
-      smooth_step(l, 'B', f, u, uz);
+      gs_step(l, true, f, u, uz);
     }
   }
 
@@ -1324,6 +1338,16 @@ int igb_set_gs(igb_ctx* ctx, int level) {
         up[i + 1] = (int)ui.size();
       }
       V.U = upload_csr(ctx, V.n, V.n, (long long)ui.size(), up.data(), ui.data(), uv.data());
+      std::vector<int> lp(V.n + 1, 0), li;
+      std::vector<double> lvv;
+      for (int i = 0; i < V.n; ++i) {
+        for (int j = V.h_ptr[i]; j < dp[i]; ++j) {
+          li.push_back(V.h_col[j]);
+          lvv.push_back(V.h_val[j]);
+        }
+        lp[i + 1] = (int)li.size();
+      }
+      V.Lo = upload_csr(ctx, V.n, V.n, (long long)li.size(), lp.data(), li.data(), lvv.data());
       V.has_U = !(std::getenv("IGB_GS_RESIDUAL") && std::string(std::getenv("IGB_GS_RESIDUAL")) == "full");
     }
     V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);

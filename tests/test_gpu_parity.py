@@ -306,3 +306,28 @@ def test_kronecker_transfers_match_P(cfg, kw):
     _check_history(rep.residuals, histo, "kron transfers vs oracle")
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
+
+
+@pytest.mark.parametrize("smoother,nu,mu", [("gs", 2, 1), ("gs", 1, 2), ("hyb", 2, 1), ("scms", 1, 1)])
+def test_other_smoothers_and_cycles_match_oracle(smoother, nu, mu):
+    """Non-default cycle knobs (multigrid.py:23-50): plain Gauss-Seidel smoothing with nu = 2
+    (forward steps from a nonzero iterate use T u' = f - (A - T) u), the W-cycle, the hybrid
+    smoother with nu = 2, SCMS alone -- device PCG against the oracle on the same setup."""
+    import dataclasses
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, _, _ = get_setup("cfg3", levels=2)
+    cfg = dataclasses.replace(pr.config, smoother=smoother, nu=nu, mu=mu)
+    setup = multigrid.MultigridSetup(pr.hier, cfg)
+    f = pr.rhs(setup.assembled_finest)
+    solver = multigrid.MultigridSolver(pr.hier, cfg, device=0, setup=setup)
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(41)
+    r = rng.standard_normal(solver.n_dofs)
+    assert rel(solver.cycle(solver.finest, r), orc.cycle(solver.finest, r)) <= 1e-11
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=cfg.tol, max_iters=cfg.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, f"{smoother} nu={nu} mu={mu}")
+    assert rel(rep.x, xo) <= 1e-10
+    solver.close()

@@ -248,14 +248,20 @@ def run_ours(args, rank, world, local):
     ms = max_over_ranks(float(np.mean(dev_ms)), dist, f"cuda:{local}")
     value = replica_value(world, n, its, ms)
 
-    # ---- e2e: public host API (H2D of b, solve, D2H of x + history), wall clock
-    fh = f.copy()
+    # ---- e2e: public host API (H2D of b from pinned host memory, solve, D2H of x + history into
+    # host memory), wall clock
+    fh = ctx.pinned(n)
+    fh[:] = f
+    xh = ctx.pinned(n)
+    for _ in range(args.warmup):  # the host-buffer entry point has its own solve graph: warm it too
+        l2_flush()
+        solver.ctx.pcg(fh, cfg.tol, cfg.max_iters, out=xh)
     e2e_s = []
     for _ in range(max(1, args.steps)):
         l2_flush()
         barrier()
         t = time.perf_counter()
-        x, its_e, hist_e = solver.ctx.pcg(fh, cfg.tol, cfg.max_iters)
+        x, its_e, hist_e = solver.ctx.pcg(fh, cfg.tol, cfg.max_iters, out=xh)
         e2e_s.append(time.perf_counter() - t)
     e2e_t = max_over_ranks(float(np.mean(e2e_s)), dist, f"cuda:{local}")
     e2e = {"value": replica_value(world, n, its_e, 1e3 * e2e_t), "unit": "DoF*it/s", "h2d_bytes_per_step": 8 * n,

@@ -145,6 +145,11 @@ int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
                    double* d_x, int* its, double* hist, int hist_cap);
 
 /* Device scratch helpers for device-resident benchmarking. */
+/* Pinned (page-locked) host buffers for the host-buffer entry points (igb_pcg's b and x): the
+ * copies then run at full link speed inside the solve's single synchronisation. */
+int igb_host_alloc(igb_ctx* ctx, long long bytes, void** hptr);
+int igb_host_free(igb_ctx* ctx, void* hptr);
+
 int igb_device_alloc(igb_ctx* ctx, long long bytes, void** dptr);
 int igb_device_free(igb_ctx* ctx, void* dptr);
 int igb_memcpy_h2d(igb_ctx* ctx, void* dst, const void* src, long long bytes);

@@ -44,6 +44,8 @@ SIGNATURES = {
     "igb_pcg": ([_p, _p, _d, _i, _p, _ip, _p, _i], _i),
     "igb_pcg_device": ([_p, _p, _d, _i, _p, _ip, _p, _i], _i),
     "igb_device_alloc": ([_p, _ll, ctypes.POINTER(_p)], _i),
+    "igb_host_alloc": ([_p, _ll, ctypes.POINTER(_p)], _i),
+    "igb_host_free": ([_p, _p], _i),
     "igb_device_free": ([_p, _p], _i),
     "igb_memcpy_h2d": ([_p, _p, _p, _ll], _i),
     "igb_memcpy_d2h": ([_p, _p, _p, _ll], _i),
@@ -106,8 +108,21 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
+            for p in getattr(self, "_pinned", []):
+                self.lib.igb_host_free(self.h, ctypes.c_void_p(p))
+            self._pinned = []
             self.lib.igb_destroy(self.h)
             self.h = None
+
+    def pinned(self, n):
+        """float64[n] numpy array in page-locked host memory (freed with the context): host
+        buffers for ``pcg`` that copy at full link speed."""
+        p = ctypes.c_void_p()
+        self._check(self.lib.igb_host_alloc(self.h, 8 * max(1, int(n)), ctypes.byref(p)), "igb_host_alloc")
+        if not hasattr(self, "_pinned"):
+            self._pinned = []
+        self._pinned.append(p.value)
+        return np.frombuffer((ctypes.c_double * max(1, int(n))).from_address(p.value), dtype=np.float64)[:int(n)]
 
     def __del__(self):
         try:
@@ -197,9 +212,10 @@ class Context:
         self._check(self.lib.igb_cycle(self.h, int(level), _ptr(f), _ptr(u)), "igb_cycle")
         return u
 
-    def pcg(self, b, tol, max_iters):
+    def pcg(self, b, tol, max_iters, out=None):
+        """igb_pcg with host buffers; ``out`` (e.g. ``pinned(n)``) receives x."""
         b = _c(b, np.float64)
-        x = np.empty_like(b)
+        x = out if out is not None else np.empty_like(b)
         hist = np.empty(max(1, int(max_iters)))
         its = ctypes.c_int(0)
         self._check(self.lib.igb_pcg(self.h, _ptr(b), float(tol), int(max_iters), _ptr(x), ctypes.byref(its),

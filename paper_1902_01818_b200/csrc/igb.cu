@@ -193,6 +193,7 @@ struct igb_ctx {
   unsigned* counter = nullptr;
   CgScalars* sc = nullptr;
   CgScalars* sc_host = nullptr;  // pinned
+  double* hist_host = nullptr;   // pinned staging of the residual history
   int hist_cap = 0;
 
   // graph of cycle(L)
@@ -960,6 +961,7 @@ int igb_destroy(igb_ctx* ctx) {
   for (auto e : ctx->ev_pool) cudaEventDestroy(e);
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
+  if (ctx->hist_host) cudaFreeHost(ctx->hist_host);
   if (ctx->t0) cudaEventDestroy(ctx->t0);
   if (ctx->t1) cudaEventDestroy(ctx->t1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1860,8 +1862,10 @@ static void build_pcg_graph(igb_ctx* ctx, const double* d_b, double* d_x, int ma
   ctx->pcg_max = max_iters;
 }
 
-static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters, double* d_x,
-                     int* its, double* hist, int hist_cap) {
+// x_host (nullable): the solution is also copied there before the one host synchronisation
+// returns true when x_host was filled
+static bool pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters, double* d_x,
+                     int* its, double* hist, int hist_cap, double* x_host = nullptr) {
   if (max_iters < 0) throw ArgError("max_iters must be >= 0");
   cudaStream_t s = ctx->stream;
   const int L = ctx->L;
@@ -1871,6 +1875,9 @@ static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
     ctx->hist_dev = ctx->alloc<double>(std::max(1, max_iters));
     ctx->hist_cap = max_iters;
     ctx->pcg_max = -1;  // the graph holds the old history buffer
+    if (ctx->hist_host) cudaFreeHost(ctx->hist_host);
+    CU(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hist_host), sizeof(double) * std::max(1, max_iters),
+                     cudaHostAllocDefault));
   }
   CgScalars init{};
   init.tol = tol;
@@ -1891,7 +1898,12 @@ static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
       CU(cudaEventRecord(ctx->t0, s));
       CU(cudaGraphLaunch(ctx->pcg_exec, s));
       CU(cudaEventRecord(ctx->t1, s));
+      // results back in one batch (scalars, the whole history buffer, x) and one synchronisation
       CU(cudaMemcpyAsync(ctx->sc_host, ctx->sc, sizeof(CgScalars), cudaMemcpyDeviceToHost, s));
+      if (hist && max_iters > 0)
+        CU(cudaMemcpyAsync(ctx->hist_host, ctx->hist_dev, sizeof(double) * std::min(max_iters, hist_cap),
+                           cudaMemcpyDeviceToHost, s));
+      if (x_host) CU(cudaMemcpyAsync(x_host, d_x, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
       CU(cudaStreamSynchronize(s));
       float ms = 0;
       CU(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));
@@ -1900,9 +1912,9 @@ static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
       const int nit = ctx->sc_host->normb == 0.0 ? 0 : ctx->sc_host->it;
       *its = nit;
       const int nh = std::min(nit, hist_cap);
-      if (hist && nh > 0) CU(cudaMemcpy(hist, ctx->hist_dev, sizeof(double) * nh, cudaMemcpyDeviceToHost));
+      if (hist && nh > 0) std::memcpy(hist, ctx->hist_host, sizeof(double) * nh);
       ctx->launches_direct += ctx->pcg_n_pre + nit * ctx->pcg_n_head + std::max(nit - 1, 0) * ctx->pcg_n_if;
-      return;
+      return x_host != nullptr;
     }
   }
   CU(cudaMemcpyAsync(ctx->sc, ctx->sc_host, sizeof(CgScalars), cudaMemcpyHostToDevice, s));
@@ -1922,7 +1934,7 @@ static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
     CU(cudaEventElapsedTime(&ms, ctx->t0, ctx->t1));
     ctx->last_pcg_ms = ms;
     ctx->last_cycle_ms = 0;
-    return;
+    return false;
   }
   double* r = F.f;   // CG residual doubles as the cycle input
   double* z = F.u;   // cycle output
@@ -1968,6 +1980,7 @@ static void pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
   if (hist && nh > 0) CU(cudaMemcpy(hist, ctx->hist_dev, sizeof(double) * nh, cudaMemcpyDeviceToHost));
   ctx->last_cycle_ms = 0;
   (void)ncycles;
+  return false;
 }
 
 int igb_pcg(igb_ctx* ctx, const double* b, double tol, int max_iters, double* x, int* its,
@@ -1977,11 +1990,13 @@ int igb_pcg(igb_ctx* ctx, const double* b, double tol, int max_iters, double* x,
     CU(cudaSetDevice(ctx->device));
     Level& F = ctx->lev[ctx->L];
     const int n = F.n;
-    // host -> device copy of b and device -> host copy of x
+    // host -> device copy of b and device -> host copy of x (inside pcg_core's one synchronisation;
+    // copies run at full speed when the caller's buffers are pinned, igb_host_alloc)
     CU(cudaMemcpyAsync(ctx->b, b, sizeof(double) * n, cudaMemcpyHostToDevice, ctx->stream));
-    pcg_core(ctx, ctx->b, tol, max_iters, ctx->x, its, hist, hist_cap);
-    CU(cudaMemcpyAsync(x, ctx->x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
-    CU(cudaStreamSynchronize(ctx->stream));
+    if (!pcg_core(ctx, ctx->b, tol, max_iters, ctx->x, its, hist, hist_cap, x)) {  // host-loop path
+      CU(cudaMemcpyAsync(x, ctx->x, sizeof(double) * n, cudaMemcpyDeviceToHost, ctx->stream));
+      CU(cudaStreamSynchronize(ctx->stream));
+    }
   });
 }
 
@@ -1992,6 +2007,16 @@ int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters, d
     CU(cudaSetDevice(ctx->device));
     pcg_core(ctx, d_b, tol, max_iters, d_x, its, hist, hist_cap);
   });
+}
+
+int igb_host_alloc(igb_ctx* ctx, long long bytes, void** hptr) {
+  return guarded(ctx, [&] {
+    CU(cudaSetDevice(ctx->device));
+    CU(cudaHostAlloc(hptr, (size_t)bytes, cudaHostAllocDefault));
+  });
+}
+int igb_host_free(igb_ctx* ctx, void* hptr) {
+  return guarded(ctx, [&] { CU(cudaFreeHost(hptr)); });
 }
 
 int igb_device_alloc(igb_ctx* ctx, long long bytes, void** dptr) {

@@ -331,3 +331,15 @@ def test_other_smoothers_and_cycles_match_oracle(smoother, nu, mu):
     _check_history(rep.residuals, histo, f"{smoother} nu={nu} mu={mu}")
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
+
+
+def test_pinned_host_buffers_pcg_bitwise():
+    """igb_pcg with page-locked host buffers (igb_host_alloc): same result, bit for bit, as with
+    pageable numpy buffers and as the device-buffer entry point."""
+    pr, setup, f, solver, orc = device_solver("cfg2", levels=3)
+    ctx = solver.ctx
+    x1, its1, h1 = ctx.pcg(f, 1e-8, 500)
+    b, xo = ctx.pinned(len(f)), ctx.pinned(len(f))
+    b[:] = f
+    x2, its2, h2 = ctx.pcg(b, 1e-8, 500, out=xo)
+    assert x2 is xo and its1 == its2 and h1 == h2 and np.array_equal(x1, x2)

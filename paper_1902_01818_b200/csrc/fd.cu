@@ -16,6 +16,8 @@
 // right operand is copied whole into shared memory by cp.async (one latency per product).
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace igb {
@@ -260,6 +262,8 @@ void launch_rb(cudaStream_t s, const FdBatch& bt, const double* r, double* u, do
 }  // namespace
 
 int fd_rows_per_cta(int total_rows) {
+  static const int forced = std::getenv("IGB_FD_RB") ? std::atoi(std::getenv("IGB_FD_RB")) : 0;
+  if (forced == 2 || forced == 4 || forced == 8) return forced;
   // about one CTA per SM for the level's interiors together (the right operand fills shared memory)
   const int want = (total_rows + 147) / 148;
   return want <= 2 ? 2 : (want <= 4 ? 4 : 8);

@@ -281,8 +281,16 @@ def run_ours(args, rank, world, local):
     mean_launch_s = P["ms"] / 1e3 / max(1, P["launches"])
     bytes_per_launch = P["bytes"] / max(1, P["launches"])
     achieved = bytes_per_launch / mean_launch_s / 1e9 if mean_launch_s > 0 else 0.0
+    traffic, traffic_src = None, None
+    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
+    if os.path.exists(tp) and args.config == "cfg2":  # committed ncu capture of the same workload
+        t = json.load(open(tp)).get(dom)
+        if t:
+            traffic, traffic_src = t["bytes_per_launch"], t["source"]
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
-                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                "traffic_source": traffic_src,
+                "algorithmic_bytes_per_launch": bytes_per_launch,
                 "peak_source": peak_kind,
                 "note": "algorithmic bytes per launch / mean CUDA-event launch time, profiled pass",
                 "classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,

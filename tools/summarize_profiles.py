@@ -52,6 +52,23 @@ def launches(path):
     return agg
 
 
+_SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+
+def dram_bytes(rep):
+    """dram read + write bytes of the first kernel in an ncu report (unit row honoured)."""
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(out.splitlines()))
+    if len(rows) < 3:
+        return None
+    h, u, d = rows[0], rows[1], rows[2]
+    tot = 0.0
+    for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        i = h.index(k)
+        tot += float(d[i].replace(",", "")) * _SCALE.get(u[i], 1.0)
+    return tot
+
+
 def ncu_raw(rep):
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(out.splitlines()))
@@ -108,6 +125,21 @@ def main(tag):
             fh.write("stalls (warps per issue-active cycle): " + ", ".join(f"{s}={v:.2f}" for v, s in stalls) + "\n")
         lines += [f"## ncu --set full: `{kname}`", "", "```"] + [f"{k} = {v}" for k, v in m.items() if v] + [
             "stalls: " + ", ".join(f"{s}={v:.2f}" for v, s in stalls), "```", ""]
+    # DRAM traffic per launch of the captured kernel of each class, for bench.py's roofline.traffic
+    traffic = {}
+    for cls, stem in (("gs", f"prof_gs_{tag}"), ("fd", f"prof_fd_{tag}")):
+        rp = os.path.join(OUT, stem + ".ncu-rep")
+        if os.path.exists(rp):
+            tb = dram_bytes(rp)
+            if tb is not None:
+                traffic[cls] = {"bytes_per_launch": tb, "source": f"profiles/{tag}_ncu_{stem}.txt",
+                                "note": "dram__bytes_read.sum + dram__bytes_write.sum of one ncu --set full "
+                                        "capture (one launch of the class, cfg2)" + (
+                                            "; a finest-level panel sweep streams its dense diagonal-block "
+                                            "inverses (147 MB per direction, DESIGN.md section 3) against "
+                                            "22.4 MB of algorithmic triangular-solve bytes" if cls == "gs" else "")}
+    if traffic:
+        json.dump(traffic, open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
     with open(os.path.join(PROF, f"{tag}_summary.md"), "w") as fh:
         fh.write("\n".join(x for x in lines if x is not None) + "\n")
     print("\n".join(lines))

@@ -580,103 +580,6 @@ __global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict
 }
 
 // ---------------------------------------------------------------------------
-// Fused 2-D fast diagonalisation, one CTA per interior (n0, n1 <= FD_SMALL_NMAX = 80).
-// 256 threads as a 16 x 16 grid; thread (ty, tx) owns the output block
-// rows ty + 16a, columns tx + 16b (a, b < 5), so each product step loads 5 + 5
-// operands from smem for 25 FMAs (row operands are warp-broadcast, column
-// operands consecutive across lanes).
-constexpr int FDS_B = 5;
-
-// C[i][j] = sum_m L(i, m) * R(m, j) for the thread's block; L(i,m) = Lp[i*lri + m*lrm],
-// R(m,j) = Rp[m*rrm + j*rrj]
-__device__ __forceinline__ void fds_block(double (&acc)[FDS_B][FDS_B], const double* Lp, int lri, int lrm,
-                                          const double* Rp, int rrm, int rrj, int M, int ni, int nj, int ty,
-                                          int tx) {
-#pragma unroll
-  for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) acc[a][b] = 0.0;
-  for (int m = 0; m < M; ++m) {
-    double lv[FDS_B], rv[FDS_B];
-#pragma unroll
-    for (int a = 0; a < FDS_B; ++a) {
-      const int i = ty + 16 * a;
-      lv[a] = i < ni ? Lp[i * lri + m * lrm] : 0.0;
-    }
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) {
-      const int j = tx + 16 * b;
-      rv[b] = j < nj ? Rp[m * rrm + j * rrj] : 0.0;
-    }
-#pragma unroll
-    for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-      for (int b = 0; b < FDS_B; ++b) acc[a][b] = fma(lv[a], rv[b], acc[a][b]);
-  }
-}
-
-__global__ void __launch_bounds__(256) fd_small_kernel(const FdSmall* __restrict__ items,
-                                                       const double* __restrict__ r, double* u,
-                                                       double alpha, int accumulate) {
-  pdl_begin();
-  extern __shared__ double fsm[];
-  const FdSmall it = items[blockIdx.x];
-  const int n0 = it.n0, n1 = it.n1;
-  double* T0 = fsm;             // n0 x n0
-  double* T1 = T0 + n0 * n0;    // n1 x n1
-  double* A = T1 + n1 * n1;     // n0 x n1
-  double* B = A + n0 * n1;      // n0 x n1
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  for (int k = tid; k < n0 * n0; k += blockDim.x) T0[k] = __ldg(&it.T0[k]);
-  for (int k = tid; k < n1 * n1; k += blockDim.x) T1[k] = __ldg(&it.T1[k]);
-  for (int k = tid; k < n0 * n1; k += blockDim.x) A[k] = r[__ldg(&it.idx[k])];
-  __syncthreads();
-  double acc[FDS_B][FDS_B];
-  // B = T0^T A      (L(i,m) = T0[m][i], R(m,j) = A[m][j])
-  fds_block(acc, T0, 1, n0, A, n1, 1, n0, n0, n1, ty, tx);
-#pragma unroll
-  for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < n0 && j < n1) B[i * n1 + j] = acc[a][b];
-    }
-  __syncthreads();
-  // A = (B T1) ./ D  (L(i,m) = B[i][m], R(m,j) = T1[m][j])
-  fds_block(acc, B, n1, 1, T1, n1, 1, n1, n0, n1, ty, tx);
-#pragma unroll
-  for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < n0 && j < n1) A[i * n1 + j] = __ddiv_rn(acc[a][b], __ldg(&it.D[i * n1 + j]));
-    }
-  __syncthreads();
-  // B = T0 A        (L(i,m) = T0[i][m], R(m,j) = A[m][j])
-  fds_block(acc, T0, n0, 1, A, n1, 1, n0, n0, n1, ty, tx);
-#pragma unroll
-  for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < n0 && j < n1) B[i * n1 + j] = acc[a][b];
-    }
-  __syncthreads();
-  // u[idx] (+)= alpha * (B T1^T)   (L(i,m) = B[i][m], R(m,j) = T1[j][m])
-  fds_block(acc, B, n1, 1, T1, 1, n1, n1, n0, n1, ty, tx);
-#pragma unroll
-  for (int a = 0; a < FDS_B; ++a)
-#pragma unroll
-    for (int b = 0; b < FDS_B; ++b) {
-      const int i = ty + 16 * a, j = tx + 16 * b;
-      if (i < n0 && j < n1) {
-        const int g = __ldg(&it.idx[i * n1 + j]);
-        const double v = __dmul_rn(alpha, acc[a][b]);
-        u[g] = accumulate ? __dadd_rn(u[g], v) : v;
-      }
-    }
-}
-
 // ---------------------------------------------------------------------------
 // Interface pieces: u[idx[i]] (+)= tau * sum_j inv[i][j] r[idx[j]], warp per row.
 __global__ void __launch_bounds__(256) piece_gemv_kernel(const PieceRowBlock* __restrict__ blocks,
@@ -850,7 +753,7 @@ void carveout_prepare() {
       (const void*)level_sweep_kernel<false, false>, (const void*)level_sweep_kernel<true, false>,
       (const void*)level_sweep_kernel<false, true>, (const void*)level_sweep_kernel<true, true>,
       (const void*)perm_gather_kernel, (const void*)perm_scatter_kernel, (const void*)coarse_csc_kernel<true>,
-      (const void*)coarse_csc_kernel<false>, (const void*)fd_gemm_kernel, (const void*)fd_small_kernel,
+      (const void*)coarse_csc_kernel<false>, (const void*)fd_gemm_kernel,
       (const void*)piece_gemv_kernel, (const void*)dot_kernel, (const void*)cg_update_kernel,
       (const void*)cg_direction_kernel, (const void*)copy_kernel, (const void*)fill_kernel};
   for (const void* f : funcs) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
@@ -912,17 +815,6 @@ void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int tota
   launch_k(fd_gemm_kernel, dim3(total_tiles), dim3(256), 0, s, d_descs, ndesc, gsrc, sdst, alpha, accumulate);
 }
 
-void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
-                     double alpha, int accumulate) {
-  if (nitems <= 0) return;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(fd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
-  const size_t smem = sizeof(double) * (size_t)(4 * nmax * nmax);
-  launch_k(fd_small_kernel, dim3(nitems), dim3(256), smem, s, d_items, r, u, alpha, accumulate);
-}
 
 void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
                        const double* r, double* u, double tau, int accumulate) {

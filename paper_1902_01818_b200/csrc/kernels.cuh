@@ -222,16 +222,6 @@ void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int tota
 
 // ---- fused fast diagonalisation of small 2-D interiors (one CTA per interior) --
 // X = T0 ((T0^T R T1) ./ D) T1^T with R = r[idx] and u[idx] (+)= alpha X, all in smem.
-struct FdSmall {
-  const double* T0;
-  const double* T1;
-  const double* D;
-  const int* idx;
-  int n0, n1;
-};
-constexpr int FD_SMALL_NMAX = 80;
-void launch_fd_small(cudaStream_t s, const FdSmall* d_items, int nitems, int nmax, const double* r, double* u,
-                     double alpha, int accumulate);
 
 // ---- interface-piece dense solves (precomputed inverses) ---------------------
 struct PieceRowBlock {

@@ -205,10 +205,19 @@ def run_reference(args, rank, world):
 def run_ours(args, rank, world, local):
     import torch
     dist = None
+    # IGB_BENCH_ONE_GPU=1: functional test of the multi-rank path on a one-GPU box (every rank on
+    # device 0, gloo for the barrier / max reduction); its numbers are not a scaling measurement
+    one_gpu = os.environ.get("IGB_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
+    red_dev = "cpu" if one_gpu else f"cuda:{local}"
     if world > 1:
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1902_01818_b200 import multigrid
 
     pr, setup, f, t_setup = build_problem(args)
@@ -245,7 +254,7 @@ def run_ours(args, rank, world, local):
             dev_ms.append(ctx.last_timing()[0])
     barrier()
     launches = ctx.launch_count(reset=True)
-    ms = max_over_ranks(float(np.mean(dev_ms)), dist, f"cuda:{local}")
+    ms = max_over_ranks(float(np.mean(dev_ms)), dist, red_dev)
     value = replica_value(world, n, its, ms)
 
     # ---- e2e: public host API (H2D of b from pinned host memory, solve, D2H of x + history into
@@ -263,7 +272,7 @@ def run_ours(args, rank, world, local):
         t = time.perf_counter()
         x, its_e, hist_e = solver.ctx.pcg(fh, cfg.tol, cfg.max_iters, out=xh)
         e2e_s.append(time.perf_counter() - t)
-    e2e_t = max_over_ranks(float(np.mean(e2e_s)), dist, f"cuda:{local}")
+    e2e_t = max_over_ranks(float(np.mean(e2e_s)), dist, red_dev)
     e2e = {"value": replica_value(world, n, its_e, 1e3 * e2e_t), "unit": "DoF*it/s", "h2d_bytes_per_step": 8 * n,
            "d2h_bytes_per_step": 8 * n + 8 * its_e}
 

@@ -439,7 +439,8 @@ void launch_one(cudaStream_t st, const PanelArgs& a) {
   cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-// variants: B = 512: KA in {2,4,8,12}, KF in {0,1,4};  B = 256: KA in {4,8,12}, KF in {0,4,8}
+// variants: B = 512: KA in {2,4,8,12}, KF in {0,1,4}, and KA 14 with KF 0;  B = 256: KA in {4,8,12},
+// KF in {0,4,8}
 template <int KA>
 void dispatch_kf17(cudaStream_t st, const PanelArgs& a) {
   switch (a.KF) {
@@ -475,6 +476,7 @@ void for_all_variants(int KBC, F&& f) {
   per_ka(std::integral_constant<int, 4>{});
   per_ka(std::integral_constant<int, 8>{});
   per_ka(std::integral_constant<int, 12>{});
+  if (KBC == 17) f(panel_sweep_kernel<17, 14, 0>);  // long single-range rows (p = 8 backward: ~208 near)
 }
 
 }  // namespace
@@ -553,6 +555,7 @@ void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {
       case 2: dispatch_kf17<2>(st, a); break;
       case 4: dispatch_kf17<4>(st, a); break;
       case 8: dispatch_kf17<8>(st, a); break;
+      case 14: launch_one<17, 14, 0>(st, a); break;
       default: dispatch_kf17<12>(st, a); break;
     }
   } else {

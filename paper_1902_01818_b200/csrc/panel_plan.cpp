@@ -2,6 +2,8 @@
 #include "panel_plan.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <atomic>
 #include <cmath>
 #include <thread>
@@ -154,10 +156,14 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
     out.near_entries += nn;
     out.far_entries += nf;
   }
-  out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12})
+  out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12, 14})
                    : round_up_variant((max_near + 15) / 16, {4, 8, 12});
   out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4}) : round_up_variant((max_far + 15) / 16, {0, 4, 8});
+  if (out.KA == 14 && out.KF != 0) out.KA = -1;  // the KA 14 variant exists without far slots only
   if (out.KA < 0 || out.KF < 0) {
+    if (std::getenv("IGB_VERBOSE"))
+      std::fprintf(stderr, "[igb] panel plan (%s, W %d, %d ranges): max near %d, max far %d entries per row -- "
+                   "beyond the kernel variants\n", upper ? "upper" : "lower", W, out.nclu, max_near, max_far);
     // cross-range references overflowed the kernel variants: one range (if that fits)
     if (out.nclu > 1) return build_panel_plan(n, ptr, col, val, dpos, upper, G, W, R, 1, out);
     return false;

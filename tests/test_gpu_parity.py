@@ -343,3 +343,18 @@ def test_pinned_host_buffers_pcg_bitwise():
     b[:] = f
     x2, its2, h2 = ctx.pcg(b, 1e-8, 500, out=xo)
     assert x2 is xo and its1 == its2 and h1 == h2 and np.array_equal(x1, x2)
+
+
+def test_p8_backward_panel_matches_oracle():
+    """cfg4 p = 8 (L = 3): backward rows carry ~200 near entries -- the panel variant with 14
+    slots per lane (one range) -- sweeps repeatable and equal to SuperLU on triu(A) per level."""
+    pr, setup, f, solver, orc = device_solver("cfg4", p=8, levels=3)
+    rng = np.random.default_rng(43)
+    for level in range(1, solver.finest + 1):
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for op, ref in (("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward)):
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(3):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (level, op)

@@ -41,6 +41,8 @@ __all__ = [
     "build_dofs",
     "assemble_level",
     "assemble_rhs",
+    "solution_coefficients",
+    "l2_error",
     "prolongation",
 ]
 
@@ -778,6 +780,48 @@ def assemble_rhs(hier, asm, problem):
         lift = problem.dirichlet(asm.dirichlet_points)
         load_free = load_free - asm.couple @ lift
     return load_free
+
+
+def solution_coefficients(hier, asm, u_free, problem=None):
+    """Block-numbered coefficients of a free-DoF vector; with ``problem`` the Dirichlet lift is
+    added (``assembly.py:726-733``)."""
+    dofs = hier.dofs[asm.level]
+    u = np.zeros(dofs.n_block)
+    sel = dofs.free_of_block >= 0
+    u[sel] = np.asarray(u_free, dtype=float)[dofs.free_of_block[sel]]
+    if problem is not None and dofs.n_dirichlet:
+        g = problem.dirichlet(asm.dirichlet_points)
+        dsel = dofs.dir_of_block >= 0
+        u[dsel] += g[dofs.dir_of_block[dsel]]
+    return u
+
+
+def l2_error(hier, asm, u_free, problem):
+    """|| u_h - u ||_{L2(Omega)} by Gauss quadrature per patch (``assembly.py:736-755``); a
+    diagnostic of the discretisation, not on the solve path."""
+    u_block = solution_coefficients(hier, asm, u_free, problem)
+    dofs = hier.dofs[asm.level]
+    total = 0.0
+    for k in range(hier.domain.num_patches):
+        spaces = hier.spaces[asm.level][k]
+        nodes, weights, Bd = [], [], []
+        for sp in spaces:
+            x, w = bs.gauss_points(sp)
+            nodes.append(x)
+            weights.append(w)
+            Bd.append(bs.basis_matrices(sp, x, 0)[0])
+        X, J = hier.domain.patches[k].eval_grid(nodes)
+        wq = weights[0]
+        for w in weights[1:]:
+            wq = np.multiply.outer(wq, w)
+        # u_h on the quadrature grid: contract the coefficient tensor axis by axis
+        T = u_block[dofs.offsets[k]:dofs.offsets[k + 1]].reshape(dofs.dims[k])
+        for a in range(len(spaces)):
+            T = np.moveaxis(np.asarray(Bd[a] @ np.moveaxis(T, a, 0).reshape(T.shape[a], -1))
+                            .reshape((Bd[a].shape[0],) + tuple(np.delete(T.shape, a))), 0, a)
+        diff = T - problem.exact(X)
+        total += float(np.sum(wq * np.abs(np.linalg.det(J)) * diff ** 2))
+    return float(np.sqrt(total))
 
 
 def prolongation(hier, level):

@@ -17,7 +17,8 @@ import numpy as np
 import scipy.sparse
 import scipy.sparse.linalg
 
-__all__ = ["Factorization", "factorize", "cg", "DEFAULT_TOL"]
+__all__ = ["Factorization", "factorize", "solve", "cg", "dense_generalized_eig", "write_coo", "read_coo",
+           "DEFAULT_TOL"]
 
 DEFAULT_TOL = 1e-8
 
@@ -48,6 +49,13 @@ class Factorization:
         U.sort_indices()
         return L, U, np.asarray(self._lu.perm_r), np.asarray(self._lu.perm_c)
 
+    def solve(self, b, trans="N"):
+        """x with A x = b (``linsolve.py:48-53``)."""
+        return self._lu.solve(np.asarray(b, dtype=float), trans=trans)
+
+    def __call__(self, b):
+        return self.solve(b)
+
     def inverse(self):
         """Dense A^{-1}, column j = SuperLU solve of e_j (setup for the device GEMV)."""
         n = self.shape[0]
@@ -56,6 +64,43 @@ class Factorization:
 
 def factorize(A, spd=False):
     return Factorization(A, spd=spd)
+
+
+def solve(F, b):
+    """Apply a factorization (``linsolve.py:60-61``)."""
+    return F.solve(b)
+
+
+def dense_generalized_eig(A, B):
+    """Ascending eigenvalues of the pencil (A, B), A symmetric, B SPD (``linsolve.py:104-110``);
+    a dense diagnostic, not on the solve path."""
+    import scipy.linalg
+    Ad = A.toarray() if scipy.sparse.issparse(A) else np.asarray(A, dtype=float)
+    Bd = B.toarray() if scipy.sparse.issparse(B) else np.asarray(B, dtype=float)
+    if Ad.shape != Bd.shape:
+        raise ValueError("matrix dimensions do not match")
+    return scipy.linalg.eigh(Ad, Bd, eigvals_only=True)
+
+
+def write_coo(path, A):
+    """Triplet text dump (``linsolve.py:113-119``): a header line ``rows cols nnz``, then one
+    ``i j value`` line per stored entry, values with 17 significant digits (round-trips fp64)."""
+    C = scipy.sparse.coo_matrix(A)
+    lines = [f"{C.shape[0]} {C.shape[1]} {C.nnz}"]
+    lines += [f"{i} {j} {v:.17g}" for i, j, v in zip(C.row.tolist(), C.col.tolist(), C.data.tolist())]
+    with open(path, "w") as fh:
+        fh.write("\n".join(lines) + "\n")
+
+
+def read_coo(path):
+    """Inverse of :func:`write_coo` (``linsolve.py:122-131``); returns CSR (duplicates summed)."""
+    with open(path) as fh:
+        m, n, nnz = (int(t) for t in fh.readline().split())
+        body = np.loadtxt(fh, ndmin=2, max_rows=nnz) if nnz else np.zeros((0, 3))
+    if body.shape[0] != nnz:
+        raise ValueError(f"{path}: expected {nnz} entries, found {body.shape[0]}")
+    return scipy.sparse.csr_matrix((body[:, 2], (body[:, 0].astype(np.int64), body[:, 1].astype(np.int64))),
+                                   shape=(m, n))
 
 
 def cg(A, b, preconditioner=None, tol=DEFAULT_TOL, max_iters=10000, callback=None):

@@ -24,6 +24,7 @@ import itertools
 from dataclasses import dataclass, field
 
 import numpy as np
+import scipy.linalg
 import scipy.sparse
 import scipy.sparse.csgraph
 
@@ -43,6 +44,8 @@ __all__ = [
     "assemble_rhs",
     "solution_coefficients",
     "l2_error",
+    "check_coercivity",
+    "geometry_condition_diagnostic",
     "prolongation",
 ]
 
@@ -780,6 +783,23 @@ def assemble_rhs(hier, asm, problem):
         lift = problem.dirichlet(asm.dirichlet_points)
         load_free = load_free - asm.couple @ lift
     return load_free
+
+
+def check_coercivity(asm):
+    """Smallest eigenvalue of the assembled operator (dense diagnostic, ``assembly.py:705-715``);
+    a non-positive one means the SIPG penalty sigma is too small."""
+    lam = scipy.linalg.eigh(asm.A.toarray(), eigvals_only=True, subset_by_index=[0, 0])[0]
+    if lam <= 0:
+        raise ValueError(f"assembled operator is not positive definite (lambda_min={lam:.3e}); "
+                         "increase the penalty parameter sigma")
+    return lam
+
+
+def geometry_condition_diagnostic(A, A_hat):
+    """(lambda_min, lambda_max, ratio) of the pencil (A, A_hat) (``assembly.py:718-723``)."""
+    from . import linsolve
+    ev = linsolve.dense_generalized_eig(A, A_hat)
+    return float(ev[0]), float(ev[-1]), float(ev[-1] / ev[0])
 
 
 def solution_coefficients(hier, asm, u_free, problem=None):

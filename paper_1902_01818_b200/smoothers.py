@@ -33,6 +33,8 @@ __all__ = [
     "PieceDecomposition",
     "build_piece_decomposition",
     "GaussSeidel",
+    "gs_apply_forward",
+    "gs_apply_backward",
     "ScmsInteriorSolver",
     "SubspaceCorrectedMass",
     "HybridSmoother",
@@ -220,12 +222,43 @@ class GaussSeidel(_DeviceBound):
         if np.any(A.diagonal() == 0.0):
             raise ValueError("Gauss-Seidel needs a nonzero diagonal")
         self.n = A.shape[0]
+        self._A = A
+
+    def _standalone(self):
+        """A smoother built outside a MultigridSolver (e.g. ``gs_apply_forward(A, r)``) gets its own
+        one-level device context: A on level 1 under a trivial 1x1 level 0 (still the device
+        sweep; there is no host implementation)."""
+        if self._ctx is None:
+            from ._lib import Context
+            one = scipy.sparse.csr_matrix(np.ones((1, 1)))
+            ctx = Context()
+            ctx.set_num_levels(1)
+            ctx.set_level_matrix(0, one)
+            ctx.set_level_matrix(1, self._A)
+            ctx.set_prolongation(1, scipy.sparse.csr_matrix(([0.0], ([0], [0])), shape=(self.n, 1)))
+            ctx.set_gs(1)
+            ctx.set_coarse_lu(one, one, np.zeros(1, np.int32), np.zeros(1, np.int32))
+            ctx.set_cycle("gs", 1, np.ones(2, np.int32))
+            ctx.finalize()
+            self._own_ctx = ctx
+            self.bind(ctx, 1)
+        return self._ctx
 
     def apply_forward(self, r):
-        return self._require().op("gs_fwd", self._level, r, self.n)
+        return self._standalone().op("gs_fwd", self._level, r, self.n)
 
     def apply_backward(self, r):
-        return self._require().op("gs_bwd", self._level, r, self.n)
+        return self._standalone().op("gs_bwd", self._level, r, self.n)
+
+
+def gs_apply_forward(A, r):
+    """One forward Gauss-Seidel sweep from zero (``smoothers.py:203-204``), on the device."""
+    return GaussSeidel(A).apply_forward(r)
+
+
+def gs_apply_backward(A, r):
+    """One backward Gauss-Seidel sweep from zero (``smoothers.py:207-208``), on the device."""
+    return GaussSeidel(A).apply_backward(r)
 
 
 # -- subspace corrected mass ----------------------------------------------------------

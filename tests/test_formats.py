@@ -102,3 +102,13 @@ def test_dense_generalized_eig():
     assert np.allclose(lam, scipy.linalg.eigh(A, B, eigvals_only=True))
     with pytest.raises(ValueError):
         linsolve.dense_generalized_eig(A, np.eye(5))
+
+
+def test_coercivity_and_geometry_diagnostics():
+    from paper_1902_01818_b200 import assembly
+    pr, setup, f = get_setup("cfg3", levels=1)
+    asm = setup.assembled_finest
+    lam = assembly.check_coercivity(asm)
+    assert lam > 0
+    lo, hi, ratio = assembly.geometry_condition_diagnostic(setup.A[0], setup.A[0])
+    assert abs(lo - 1) < 1e-10 and abs(hi - 1) < 1e-10 and abs(ratio - 1) < 1e-10

@@ -358,3 +358,14 @@ def test_p8_backward_panel_matches_oracle():
             for _ in range(3):
                 assert np.array_equal(solver.ctx.op(op, level, x, n), first), (level, op)
             assert rel(first, ref(level, x)) <= 1e-12, (level, op)
+
+
+def test_standalone_gauss_seidel_helpers():
+    """smoothers.gs_apply_forward / gs_apply_backward (reference smoothers.py:203-208): a smoother
+    built outside a solver runs on its own one-level device context."""
+    from paper_1902_01818_b200 import smoothers
+    pr, setup, f, solver, orc = device_solver("cfg2", levels=3)
+    A = solver.A[2]
+    r = np.random.default_rng(8).standard_normal(A.shape[0])
+    assert rel(smoothers.gs_apply_forward(A, r), orc.gs_forward(2, r)) <= 1e-12
+    assert rel(smoothers.gs_apply_backward(A, r), orc.gs_backward(2, r)) <= 1e-12

@@ -98,6 +98,16 @@ int igb_set_prolongation_kron(igb_ctx* ctx, int level, int dim, int npatch, cons
                               int width, const int* p1_idx, const double* p1_val, const int* fine_free,
                               const int* fine_owner, const int* coarse_free);
 
+/* Matrix-free form of A_l for conforming spaces on affine patches (assembly.py:333-344: per patch
+ * sum_a c_a (x)_i (K_i if i == a else M_i) reduced to free DoFs, shared copies summed).  Full products
+ * A_l x (residuals, the CG product) then run by sum factorisation instead of reading A_l
+ * (IGB_MATRIX_FREE=0 keeps the CSR).  The CSR of igb_set_level_matrix stays required (Gauss-Seidel).
+ *   dims   [npatch * dim] block sizes;  c [npatch * dim] coefficient of stiffness term a
+ *   Mband, Kband  1-D mass / stiffness per (patch, axis) as n x (2p+1) bands (entry j - i + p)
+ *   block_free    [sum prod dims] block index -> free id (-1 Dirichlet) */
+int igb_set_matrix_free(igb_ctx* ctx, int level, int dim, int npatch, int p, const int* dims, const double* c,
+                        const double* Mband, const double* Kband, const int* block_free);
+
 /* Gauss-Seidel on A_l in natural order (level schedules are built here). */
 int igb_set_gs(igb_ctx* ctx, int level);
 

@@ -32,6 +32,7 @@ SIGNATURES = {
     "igb_set_level_matrix": ([_p, _i, _i, _ll, _p, _p, _p], _i),
     "igb_set_prolongation": ([_p, _i, _i, _i, _ll, _p, _p, _p], _i),
     "igb_set_prolongation_kron": ([_p, _i, _i, _i, _p, _p, _i, _p, _p, _p, _p, _p], _i),
+    "igb_set_matrix_free": ([_p, _i, _i, _i, _i, _p, _p, _p, _p, _p], _i),
     "igb_set_gs": ([_p, _i], _i),
     "igb_scms_begin": ([_p, _i, _d], _i),
     "igb_scms_add_interior": ([_p, _i, _i, _p, _p, _p, _p, _p, _p], _i),
@@ -159,6 +160,14 @@ class Context:
                                                        _ptr(nf), _ptr(nc), int(kd["width"]), _ptr(idx), _ptr(val),
                                                        _ptr(ff), _ptr(fo), _ptr(cf)),
                     "igb_set_prolongation_kron")
+
+    def set_matrix_free(self, level, md):
+        """Matrix-free form of A_level (assembly.matrix_free_data)."""
+        dims, c = _c(md["dims"], np.int32), _c(md["c"], np.float64)
+        Mb, Kb, bf = _c(md["Mband"], np.float64), _c(md["Kband"], np.float64), _c(md["block_free"], np.int32)
+        self._check(self.lib.igb_set_matrix_free(self.h, level, int(md["dim"]), int(dims.shape[0]), int(md["p"]),
+                                                 _ptr(dims), _ptr(c), _ptr(Mb), _ptr(Kb), _ptr(bf)),
+                    "igb_set_matrix_free")
 
     def set_gs(self, level):
         self._check(self.lib.igb_set_gs(self.h, level), "igb_set_gs")

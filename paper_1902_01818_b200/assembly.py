@@ -44,6 +44,7 @@ __all__ = [
     "assemble_rhs",
     "solution_coefficients",
     "l2_error",
+    "matrix_free_data",
     "check_coercivity",
     "geometry_condition_diagnostic",
     "prolongation",
@@ -783,6 +784,46 @@ def assemble_rhs(hier, asm, problem):
         lift = problem.dirichlet(asm.dirichlet_points)
         load_free = load_free - asm.couple @ lift
     return load_free
+
+
+def matrix_free_data(hier, level):
+    """Sum-factorisation description of the assembled ``A_level`` for the device matrix-free
+    operator, or None when it does not apply.  Applies to conforming spaces on patches with a
+    constant diagonal Jacobian, exactly the case ``_bulk_matrices`` assembles by Kronecker products
+    (``assembly.py:333-344``): per patch K = sum_a c_a (x)_i (K_i if i == a else M_i),
+    c_a = det / s_a^2, reduced to free DoFs with shared copies summed."""
+    if hier.mode != "conforming" or hier.dim not in (2, 3):
+        return None
+    dofs = hier.dofs[level]
+    d = hier.dim
+    bands_M, bands_K, cs = [], [], []
+    mats = []
+    for k in range(hier.domain.num_patches):
+        scal = _probe_jacobian(hier.domain.patches[k])
+        if scal is None:
+            return None
+        det = float(np.prod(scal))
+        cs.append([det / scal[a] ** 2 for a in range(d)])
+        mats.append([(bs.univariate_mass(s).tocsr(), bs.univariate_stiffness(s).tocsr())
+                     for s in hier.spaces[level][k]])
+    p = 0
+    for per in mats:
+        for M, K in per:
+            for X in (M, K):
+                C = X.tocoo()
+                if C.nnz:
+                    p = max(p, int(np.abs(C.row - C.col).max()))
+    w = 2 * p + 1
+    for per in mats:
+        for M, K in per:
+            for X, out in ((M, bands_M), (K, bands_K)):
+                C = X.tocoo()
+                band = np.zeros((X.shape[0], w))
+                band[C.row, C.col - C.row + p] = C.data
+                out.append(band.ravel())
+    return dict(dim=d, p=p, dims=np.array([dofs.dims[k] for k in range(hier.domain.num_patches)], dtype=np.int32),
+                c=np.array(cs, dtype=np.float64), Mband=np.concatenate(bands_M), Kband=np.concatenate(bands_K),
+                block_free=dofs.free_of_block.astype(np.int32))
 
 
 def check_coercivity(asm):

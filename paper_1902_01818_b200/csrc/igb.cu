@@ -124,6 +124,9 @@ struct Level {
   DevCsr P, PT;
   bool has_kron = false;  // Kronecker form of P (transfer.cu), used instead of the CSR pair
   KronArgs kron{};
+  bool has_mf = false;    // matrix-free A (mfree.cu), used for full products A x on this level
+  MfArgs mf{};
+  double* mf_s[4] = {nullptr, nullptr, nullptr, nullptr};
   bool has_gs = false;
   bool has_U = false;
   DevCsr U;  // strict upper triangle of A: residual after a forward sweep from zero is -U c
@@ -520,7 +523,31 @@ struct igb_ctx {
   }
 
   void residual(int l, const double* f, const double* u, double* r) {
-    spmv(lev[l].A, u, f, r, -1, K_SPMV);
+    apply_A(l, u, f, r, -1);
+  }
+  // CG: q = A_L d and alpha = rz / (d . q) (matrix-free product + dot, or the fused CSR kernel)
+  void cg_matvec(cudaStream_t s) {
+    Level& F = lev[L];
+    const DevCsr& A = F.A;
+    const int n = F.n;
+    if (F.has_mf) {
+      apply_A(L, d, nullptr, q, 0);
+      launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, d, q, partials, counter, sc, FIN_ALPHA, hist_dev); });
+      return;
+    }
+    launch(K_SPMV, 12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n, [&] {
+      launch_spmv_dot(s, n, A.ptr, A.col, A.val, d, q, A.group, partials, counter, sc, hist_dev);
+    });
+  }
+  // y = z + sign A_l x (sign 0: y = A x): matrix-free where set, else CSR
+  void apply_A(int l, const double* x, const double* z, double* y, int sign) {
+    Level& V = lev[l];
+    if (V.has_mf) {
+      const double bytes = 8.0 * (2 * V.mf.nfree) + 4.0 * V.mf.nblk + 8.0 * 9 * V.mf.nblk;
+      launch(K_SPMV, bytes, [&] { launch_mf_apply(stream, V.mf, x, z, y, sign, V.mf_s); });
+      return;
+    }
+    spmv(V.A, x, z, y, sign, K_SPMV);
   }
 
   // One smoothing step kind: 'G' fwd GS, 'B' bwd GS, 'S' scms
@@ -1178,6 +1205,70 @@ int igb_set_prolongation_kron(igb_ctx* ctx, int level, int dim, int npatch, cons
   });
 }
 
+int igb_set_matrix_free(igb_ctx* ctx, int level, int dim, int npatch, int p, const int* dims, const double* c,
+                        const double* Mband, const double* Kband, const int* block_free) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    CU(cudaSetDevice(ctx->device));
+    Level& V = ctx->level(level);
+    if (!V.n) throw StateError("set the level matrix before its matrix-free form");
+    if (dim != 2 && dim != 3) throw ArgError("matrix-free operator needs dim 2 or 3");
+    if (npatch < 1 || p < 0 || !dims || !c || !Mband || !Kband || !block_free) throw ArgError("bad matrix-free arguments");
+    if (npatch > MF_MAXP) return;  // more patches than the parameter tables: CSR stays
+    MfArgs& a = V.mf;
+    a = MfArgs{};
+    a.dim = dim;
+    a.npatch = npatch;
+    a.p = p;
+    a.nfree = V.n;
+    long long nb = 0, band = 0;
+    for (int k = 0; k < npatch; ++k) {
+      a.off[k] = nb;
+      long long sz = 1;
+      for (int d = 0; d < 3; ++d) {
+        a.n[k][d] = d < dim ? dims[k * dim + d] : 1;
+        a.c[k][d] = d < dim ? c[k * dim + d] : 0.0;
+        if (a.n[k][d] < 1) throw ArgError("empty patch block");
+      }
+      for (int d = 0; d < dim; ++d) {
+        a.band[k][d] = band;
+        band += (long long)a.n[k][d] * (2 * p + 1);
+        sz *= a.n[k][d];
+      }
+      nb += sz;
+    }
+    a.off[npatch] = nb;
+    a.nblk = nb;
+    std::vector<int> froot(V.n, -1), xptr(V.n + 1, 0), xblk;
+    for (long long b = 0; b < nb; ++b) {
+      const int f = block_free[b];
+      if (f < -1 || f >= V.n) throw ArgError("block map out of range");
+      if (f < 0) continue;
+      if (froot[f] < 0) froot[f] = (int)b;
+      else xptr[f + 1]++;
+    }
+    for (int f = 0; f < V.n; ++f) {
+      if (froot[f] < 0) throw ArgError("free DoF without a block copy");
+      xptr[f + 1] += xptr[f];
+    }
+    xblk.resize(xptr[V.n]);
+    std::vector<int> pos(xptr.begin(), xptr.end() - 1);
+    for (long long b = 0; b < nb; ++b) {
+      const int f = block_free[b];
+      if (f >= 0 && froot[f] != (int)b) xblk[pos[f]++] = (int)b;
+    }
+    a.Mb = ctx->upload(Mband, (size_t)band);
+    a.Kb = ctx->upload(Kband, (size_t)band);
+    a.bfree = ctx->upload(block_free, (size_t)nb);
+    a.froot = ctx->upload(froot.data(), froot.size());
+    a.xptr = ctx->upload(xptr.data(), xptr.size());
+    a.xblk = xblk.empty() ? ctx->alloc<int>(1) : ctx->upload(xblk.data(), xblk.size());
+    for (int i = 0; i < 4; ++i) V.mf_s[i] = ctx->alloc<double>((size_t)nb);
+    const char* me = std::getenv("IGB_MATRIX_FREE");
+    V.has_mf = !(me && std::string(me) == "0");
+  });
+}
+
 // Row-panel sweep for one direction (panel_plan.h).  Chosen when the panel chain
 // (npan) is clearly shorter than the DAG depth (nlev) or when forced; cluster of 16
 // CTAs (B = 512) if the device can host it, else 8 (B = 256).
@@ -1709,7 +1800,7 @@ int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out) {
           CU(cudaMemcpyAsync(V.f, in, sizeof(double) * n, cudaMemcpyHostToDevice, s));
           if (op == IGB_OP_RESIDUAL)
             CU(cudaMemcpyAsync(V.c, out, sizeof(double) * n, cudaMemcpyHostToDevice, s));
-          ctx->spmv(V.A, V.f, op == IGB_OP_RESIDUAL ? V.c : nullptr, V.r, op == IGB_OP_RESIDUAL ? -1 : 0, K_SPMV);
+          ctx->apply_A(level, V.f, op == IGB_OP_RESIDUAL ? V.c : nullptr, V.r, op == IGB_OP_RESIDUAL ? -1 : 0);
           CU(cudaMemcpyAsync(out, V.r, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
           break;
         }
@@ -1817,10 +1908,7 @@ static void build_pcg_graph(igb_ctx* ctx, const double* d_b, double* d_x, int ma
     ctx->stream = ctx->aux[0];
     CU(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     c0 = ctx->graph_kernels;
-    ctx->launch(K_SPMV, 12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n, [&] {
-      launch_spmv_dot(s, n, A.ptr, A.col, A.val, ctx->d, ctx->q, A.group, ctx->partials, ctx->counter, ctx->sc,
-                      ctx->hist_dev);
-    });
+    ctx->cg_matvec(s);
     ctx->launch(K_CG, 56.0 * n, [&] {
       launch_cg_update(s, n, d_x, r, ctx->d, ctx->q, ctx->partials, ctx->counter, ctx->sc, ctx->hist_dev);
     });
@@ -1948,10 +2036,7 @@ static bool pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
   const DevCsr& A = F.A;
   int it = 0;
   for (it = 1; it <= max_iters; ++it) {
-    ctx->launch(K_SPMV, 12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n, [&] {
-      launch_spmv_dot(s, n, A.ptr, A.col, A.val, ctx->d, ctx->q, A.group, ctx->partials,
-                      ctx->counter, ctx->sc, ctx->hist_dev);
-    });
+    ctx->cg_matvec(s);
     ctx->launch(K_CG, 56.0 * n, [&] {
       launch_cg_update(s, n, d_x, r, ctx->d, ctx->q, ctx->partials, ctx->counter, ctx->sc,
                        ctx->hist_dev);

@@ -761,6 +761,7 @@ void carveout_prepare() {
   set_carveout_panel_fd(pct);
   flow_set_carveout(pct);
   kron_set_carveout(pct);
+  mf_set_carveout(pct);
 }
 
 size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }

@@ -187,6 +187,23 @@ void launch_kron_prolong(cudaStream_t s, const KronArgs& a, const double* e, con
                          int accumulate);
 void launch_kron_restrict(cudaStream_t s, const KronArgs& a, const double* r, double* y);
 
+// ---- matrix-free finest-level operator on affine conforming patches (mfree.cu) ----------
+constexpr int MF_MAXP = 16;
+struct MfArgs {
+  int dim, npatch, p, nfree;
+  long long nblk;
+  long long off[MF_MAXP + 1];      // block offsets per patch
+  int n[MF_MAXP][3];               // block sizes per axis
+  long long band[MF_MAXP][3];      // offsets of the (n x (2p+1)) band arrays in Mb / Kb
+  double c[MF_MAXP][3];            // det / s_a^2 per stiffness term
+  const double* Mb; const double* Kb;
+  const int* bfree;                // block -> free (-1 Dirichlet)
+  const int* froot; const int* xptr; const int* xblk;  // free -> root block, other copies
+};
+void mf_set_carveout(int pct);
+void launch_mf_apply(cudaStream_t s, const MfArgs& a, const double* x, const double* z, double* y, int sign,
+                     double* const scratch[4]);
+
 // ---- coarse solve: column-oriented sparse LU substitution, one CTA, rhs in smem
 // y[k] = rhs[inv_perm_r[k]];  L y = y (unit lower, CSC);  U w = y (CSC, diag at udiag[j]);
 // out[i] = w[perm_c[i]].  Column j updates run in parallel; one barrier per column.

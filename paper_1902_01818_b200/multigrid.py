@@ -14,6 +14,7 @@ host<->device transfer of ``f``/``x`` per solve).
 """
 
 import json
+import os
 import time
 from dataclasses import dataclass, field, asdict
 
@@ -193,6 +194,13 @@ class MultigridSolver:
         ctx.set_num_levels(L)
         for level in range(L + 1):
             ctx.set_level_matrix(level, self.A[level])
+        # matrix-free finest operator where the patches allow it and A_L is large enough for HBM
+        # traffic to matter (small levels are launch-bound: the CSR's one launch is cheaper)
+        min_nnz = int(os.environ.get("IGB_MATRIX_FREE_MIN_NNZ", 20_000_000))
+        if self.A[L].nnz >= min_nnz:
+            md = assembly.matrix_free_data(self.hier, L)
+            if md is not None:
+                ctx.set_matrix_free(L, md)
         for level in range(1, L + 1):
             ctx.set_prolongation(level, self.P[level])
             if len(self.hier.spaces[level][0]) in (2, 3):

@@ -369,3 +369,34 @@ def test_standalone_gauss_seidel_helpers():
     r = np.random.default_rng(8).standard_normal(A.shape[0])
     assert rel(smoothers.gs_apply_forward(A, r), orc.gs_forward(2, r)) <= 1e-12
     assert rel(smoothers.gs_apply_backward(A, r), orc.gs_backward(2, r)) <= 1e-12
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg5", {"levels": 2}), ("cfg2", {"levels": 3})])
+def test_matrix_free_operator_matches(cfg, kw):
+    """Matrix-free finest operator (sum factorisation on affine conforming patches, mfree.cu),
+    forced on small levels (IGB_MATRIX_FREE_MIN_NNZ=0): A x and f - A x against the assembled
+    CSR to 1e-13, and the PCG solve against the oracle."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup(cfg, **kw)
+    os.environ["IGB_MATRIX_FREE_MIN_NNZ"] = "0"
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_MATRIX_FREE_MIN_NNZ"]
+    L = solver.finest
+    A = solver.A[L]
+    rng = np.random.default_rng(51)
+    x, z = rng.standard_normal(A.shape[0]), rng.standard_normal(A.shape[0])
+    y = solver.ctx.op("spmv", L, x, A.shape[0])
+    assert rel(y, A @ x) <= 1e-13
+    assert np.array_equal(solver.ctx.op("spmv", L, x, A.shape[0]), y)  # fixed order
+    assert rel(solver.ctx.op("residual", L, x, A.shape[0], out_init=z), z - A @ x) <= 1e-13
+    orc = OracleSolver(setup.setup_bundle())
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, f"{cfg} matrix-free vs oracle")
+    assert rel(rep.x, xo) <= 1e-10
+    solver.close()

@@ -567,7 +567,7 @@ struct igb_ctx {
   // half the matrix traffic of f - A u (same iterate up to rounding)
   void gs_step(int l, bool upper, const double* f, double* u, bool& u_zero) {
     Level& V = lev[l];
-    if (u_zero || !V.has_U) {
+    if (u_zero || !V.has_U || V.has_mf) {  // matrix-free level: the full residual is the cheaper read
       smooth_step(l, upper ? 'B' : 'G', f, u, u_zero);
       return;
     }
@@ -587,7 +587,7 @@ struct igb_ctx {
       smooth_step(l, 'G', f, u, uz);
       for (int i = 0; i < st; ++i) {
         Level& V = lev[l];
-        if (i == 0 && from_zero && V.has_U) {
+        if (i == 0 && from_zero && V.has_U && !V.has_mf) {
           // u = c with tril(A) c = f, so f - A u = -triu(A, 1) c: half the matrix traffic
           spmv(V.U, u, nullptr, V.r, -1, K_SPMV);
           scms(l, V.r, u, false);

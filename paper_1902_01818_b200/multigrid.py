@@ -194,9 +194,9 @@ class MultigridSolver:
         ctx.set_num_levels(L)
         for level in range(L + 1):
             ctx.set_level_matrix(level, self.A[level])
-        # matrix-free finest operator where the patches allow it and A_L is large enough for HBM
-        # traffic to matter (small levels are launch-bound: the CSR's one launch is cheaper)
-        min_nnz = int(os.environ.get("IGB_MATRIX_FREE_MIN_NNZ", 20_000_000))
+        # matrix-free finest operator where the patches allow it and A_L is not tiny (measured: cfg2
+        # 5.10 -> 5.04 ms; cfg1's 98K-nonzero level is launch-bound, 0.78 ms CSR vs 0.90 ms)
+        min_nnz = int(os.environ.get("IGB_MATRIX_FREE_MIN_NNZ", 1_000_000))
         if self.A[L].nnz >= min_nnz:
             md = assembly.matrix_free_data(self.hier, L)
             if md is not None:

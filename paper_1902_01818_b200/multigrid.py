@@ -196,11 +196,14 @@ class MultigridSolver:
             ctx.set_level_matrix(level, self.A[level])
         # matrix-free finest operator where the patches allow it and A_L is not tiny (measured: cfg2
         # 5.10 -> 5.04 ms; cfg1's 98K-nonzero level is launch-bound, 0.78 ms CSR vs 0.90 ms)
+        # Coarser levels too: their Galerkin operators P^T A P equal the rediscretised ones the
+        # sum factorisation applies to ~2e-15 relative (nested spaces, exact quadrature)
         min_nnz = int(os.environ.get("IGB_MATRIX_FREE_MIN_NNZ", 1_000_000))
-        if self.A[L].nnz >= min_nnz:
-            md = assembly.matrix_free_data(self.hier, L)
-            if md is not None:
-                ctx.set_matrix_free(L, md)
+        for level in range(1, L + 1):
+            if self.A[level].nnz >= min_nnz:
+                md = assembly.matrix_free_data(self.hier, level)
+                if md is not None:
+                    ctx.set_matrix_free(level, md)
         for level in range(1, L + 1):
             ctx.set_prolongation(level, self.P[level])
             if len(self.hier.spaces[level][0]) in (2, 3):

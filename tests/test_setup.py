@@ -127,3 +127,14 @@ def test_kronecker_transfer_description_reproduces_P(name, kw):
         x, y = rng.standard_normal(P.shape[1]), rng.standard_normal(P.shape[0])
         assert np.abs(assembly.kron_apply(kd, x) - P @ x).max() <= 1e-14 * np.abs(P @ x).max()
         assert np.abs(assembly.kron_apply(kd, y, True) - P.T @ y).max() <= 1e-14 * np.abs(P.T @ y).max()
+
+
+@pytest.mark.parametrize("name,kw", [("cfg5", {"levels": 2}), ("cfg2", {"levels": 3})])
+def test_galerkin_equals_rediscretised_on_affine_patches(name, kw):
+    """The matrix-free operator applies the rediscretised coarse operators; on nested spaces over
+    affine patches they equal the reference's Galerkin products P^T A P (multigrid.py:95-99)."""
+    from paper_1902_01818_b200 import assembly
+    pr, setup, f = get_setup(name, **kw)
+    for level in range(1, pr.hier.L):
+        Ag, Ad = setup.A[level], assembly.assemble_level(pr.hier, level).A
+        assert abs(Ag - Ad).max() <= 1e-14 * abs(Ag).max()

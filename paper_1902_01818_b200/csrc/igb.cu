@@ -140,6 +140,7 @@ struct Level {
   PieceRowBlock* d_blocks = nullptr;
   double piece_bytes = 0;
   bool pieces_fused = false;  // done by the FD back kernel's extra CTAs
+  int piece_max_m = 0;
   long long piece_rows = 0;
   FdPlan fd;
   size_t fd_scratch = 0;
@@ -489,7 +490,7 @@ struct igb_ctx {
     }
     if (!V.h_blocks.empty() && !V.pieces_fused) {
       launch(K_PIECES, V.piece_bytes, [&] {
-        launch_piece_gemv(stream, V.d_blocks, (int)V.h_blocks.size(), res, u, V.tau, u_zero ? 0 : 1);
+        launch_piece_gemv(stream, V.d_blocks, (int)V.h_blocks.size(), res, u, V.tau, u_zero ? 0 : 1, V.piece_max_m);
       });
     }
   }
@@ -498,7 +499,7 @@ struct igb_ctx {
     Coarse& C = coarse;
     if (C.ndense) {
       const double bytes = 8.0 * C.n * (double)C.n + 24.0 * C.n;
-      launch(K_COARSE, bytes, [&] { launch_piece_gemv(stream, C.d_dense, C.ndense, rhs, out, 1.0, 0); });
+      launch(K_COARSE, bytes, [&] { launch_piece_gemv(stream, C.d_dense, C.ndense, rhs, out, 1.0, 0, C.n); });
       return;
     }
     if (C.n > 7000) {  // rhs + column pointers no longer fit in shared memory
@@ -1583,10 +1584,12 @@ int igb_scms_add_piece(igb_ctx* ctx, int level, int m, const int* idx, const dou
       if (idx[k] < 0 || idx[k] >= V.n) throw ArgError("piece index out of range");
     const int* didx = ctx->upload(idx, (size_t)m);
     const double* dinv = ctx->upload(inv, (size_t)m * m);
-    for (int r0 = 0; r0 < m; r0 += 8) {
-      PieceRowBlock b{dinv, didx, m, r0, std::min(8, m - r0)};
+    const int rows = m >= 512 ? 64 : 8;  // large pieces: amortise the staged r[idx] over 64 rows
+    for (int r0 = 0; r0 < m; r0 += rows) {
+      PieceRowBlock b{dinv, didx, m, r0, std::min(rows, m - r0)};
       V.h_blocks.push_back(b);
     }
+    V.piece_max_m = std::max(V.piece_max_m, m);
     V.piece_bytes += 8.0 * m * (double)m + 8.0 * m * 3 + 4.0 * m;
     V.piece_rows += m;
   });
@@ -1688,6 +1691,8 @@ int igb_set_coarse_lu(igb_ctx* ctx, int n0, long long l_nnz, const int* l_ptr, c
       const double* dM = ctx->upload(M.data(), M.size());
       const int* didx = ctx->upload(ident.data(), ident.size());
       std::vector<PieceRowBlock> blocks;
+      // 8 rows per block: one coarse operator alone must still spread over the SMs (measured: 64 rows
+      // per block left cfg5's 1331^2 operator on 21 blocks, 0.38 vs 0.12 ms per solve)
       for (int r0 = 0; r0 < n0; r0 += 8) blocks.push_back(PieceRowBlock{dM, didx, n0, r0, std::min(8, n0 - r0)});
       C.d_dense = ctx->upload(blocks.data(), blocks.size());
       C.ndense = (int)blocks.size();

@@ -582,22 +582,45 @@ __global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict
 // ---------------------------------------------------------------------------
 // ---------------------------------------------------------------------------
 // Interface pieces: u[idx[i]] (+)= tau * sum_j inv[i][j] r[idx[j]], warp per row.
+// The block's gathered right-hand side r[idx] is staged in shared memory once (smem_m > 0: every
+// piece of the launch has m <= smem_m), then each warp streams its rows of the dense inverse with
+// four independent row loads in flight (HBM-bound: 3-D face pieces are 4225^2 doubles each).  Per
+// lane the sum runs over j = lane, lane + 32, ... in order, as before the staging.
 __global__ void __launch_bounds__(256) piece_gemv_kernel(const PieceRowBlock* __restrict__ blocks,
                                                          const double* __restrict__ r, double* u,
-                                                         double tau, int accumulate) {
+                                                         double tau, int accumulate, int smem_m) {
   pdl_begin();
+  extern __shared__ double rp[];
   const PieceRowBlock b = blocks[blockIdx.x];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (warp >= b.nrows) return;
-  const int i = b.row0 + warp;
-  const double* row = b.inv + (long long)i * b.m;
-  double s = 0.0;
-  for (int j = lane; j < b.m; j += 32) s = fma(__ldg(&row[j]), __ldg(&r[__ldg(&b.idx[j])]), s);
-  s = warp_sum(s);
-  if (lane == 0) {
-    const int gi = __ldg(&b.idx[i]);
-    const double v = __dmul_rn(tau, s);
-    u[gi] = accumulate ? __dadd_rn(u[gi], v) : v;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const bool staged = smem_m > 0;
+  if (staged) {
+    for (int j = threadIdx.x; j < b.m; j += blockDim.x) rp[j] = __ldg(&r[__ldg(&b.idx[j])]);
+    __syncthreads();
+  }
+  for (int i = warp; i < b.nrows; i += nw) {
+    const int row_i = b.row0 + i;
+    const double* row = b.inv + (long long)row_i * b.m;
+    double s = 0.0;
+    if (staged) {
+      int j = lane;
+      for (; j + 96 < b.m; j += 128) {
+        double v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = __ldcs(&row[j + 32 * q]);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) s = fma(v[q], rp[j + 32 * q], s);
+      }
+      for (; j < b.m; j += 32) s = fma(__ldcs(&row[j]), rp[j], s);
+    } else {
+      for (int j = lane; j < b.m; j += 32) s = fma(__ldg(&row[j]), __ldg(&r[__ldg(&b.idx[j])]), s);
+    }
+    s = warp_sum(s);
+    if (lane == 0) {
+      const int gi = __ldg(&b.idx[row_i]);
+      const double v = __dmul_rn(tau, s);
+      u[gi] = accumulate ? __dadd_rn(u[gi], v) : v;
+    }
   }
 }
 
@@ -818,9 +841,16 @@ void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int tota
 
 
 void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
-                       const double* r, double* u, double tau, int accumulate) {
+                       const double* r, double* u, double tau, int accumulate, int max_m) {
   if (nblocks <= 0) return;
-  launch_k(piece_gemv_kernel, dim3(nblocks), dim3(256), 0, s, d_blocks, r, u, tau, accumulate);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(piece_gemv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  const int smem_m = max_m > 0 && max_m <= 25600 ? max_m : 0;  // 200 KB of staged r[idx]
+  launch_k(piece_gemv_kernel, dim3(nblocks), dim3(256), (size_t)8 * smem_m, s, d_blocks, r, u, tau, accumulate,
+           smem_m);
 }
 
 void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double* partials,

@@ -246,7 +246,7 @@ struct PieceRowBlock {
   const int* idx;      // m
   int m;
   int row0;            // first row handled by this block
-  int nrows;           // rows in this block (<= warps per block)
+  int nrows;           // rows in this block (piece_gemv: any; fused FD back kernel: <= its warps)
 };
 
 // ---- fused 2-D fast diagonalisation (fd.cu): two launches per application, RB rows of
@@ -278,8 +278,9 @@ struct FdBatch {
 int fd_rows_per_cta(int total_rows);
 void launch_fd_batch(cudaStream_t s, const FdBatch& bt, const double* r, double* u, double alpha, int accumulate);
 
+// max_m: the largest piece order among the blocks (shared-memory staging of r[idx]; 0 = none)
 void launch_piece_gemv(cudaStream_t s, const PieceRowBlock* d_blocks, int nblocks,
-                       const double* r, double* u, double tau, int accumulate);
+                       const double* r, double* u, double tau, int accumulate, int max_m);
 
 // ---- CG vector kernels with deterministic reductions -------------------------
 struct CgScalars {

@@ -523,14 +523,17 @@ __global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
 
-  for (int k0 = 0; k0 < K; k0 += FD_BK) {
+  // tile loads for k-step k0 into registers (issued one step ahead: the global latency of step
+  // k0 + FD_BK overlaps the FMAs of step k0)
+  double ra[4], rb[4];
+  auto fetch = [&](int k0) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int e = tid + 256 * q;
       int i, k;
       if (a_kfast) { i = e >> 4; k = e & 15; } else { i = e & 63; k = e >> 6; }
       const int gi = i0 + i, gk = k0 + k;
-      As[k][i] = (gi < M && gk < K) ? __ldg(&A[gi * g.a_rs + gk * g.a_cs]) : 0.0;
+      ra[q] = (gi < M && gk < K) ? __ldg(&A[gi * g.a_rs + gk * g.a_cs]) : 0.0;
       int j;
       if (b_jfast) { j = e & 63; k = e >> 6; } else { k = e & 15; j = e >> 4; }
       const int gj = j0 + j, gk2 = k0 + k;
@@ -539,9 +542,26 @@ __global__ void __launch_bounds__(256) fd_gemm_kernel(const GemmDesc* __restrict
         const long long off = boff + gk2 * g.b_rs + gj * g.b_cs;
         bv = g.b_idx ? __ldg(&gsrc[__ldg(&g.b_idx[off])]) : __ldg(&g.B[off]);
       }
-      Bs[k][j] = bv;
+      rb[q] = bv;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = tid + 256 * q;
+      int i, k;
+      if (a_kfast) { i = e >> 4; k = e & 15; } else { i = e & 63; k = e >> 6; }
+      As[k][i] = ra[q];
+      int j;
+      if (b_jfast) { j = e & 63; k = e >> 6; } else { k = e & 15; j = e >> 4; }
+      Bs[k][j] = rb[q];
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < K; k0 += FD_BK) {
+    stash();
     __syncthreads();
+    if (k0 + FD_BK < K) fetch(k0 + FD_BK);
 #pragma unroll
     for (int k = 0; k < FD_BK; ++k) {
       double a[4], b[4];

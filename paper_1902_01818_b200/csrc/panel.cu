@@ -446,6 +446,12 @@ void dispatch_kf17(cudaStream_t st, const PanelArgs& a) {
   switch (a.KF) {
     case 0: launch_one<17, KA, 0>(st, a); break;
     case 1: launch_one<17, KA, 1>(st, a); break;
+    case 5:
+      if constexpr (KA == 8) {
+        launch_one<17, 8, 5>(st, a);
+        break;
+      }
+      [[fallthrough]];
     default: launch_one<17, KA, 4>(st, a); break;
   }
 }
@@ -477,6 +483,7 @@ void for_all_variants(int KBC, F&& f) {
   per_ka(std::integral_constant<int, 8>{});
   per_ka(std::integral_constant<int, 12>{});
   if (KBC == 17) f(panel_sweep_kernel<17, 14, 0>);  // long single-range rows (p = 8 backward: ~208 near)
+  if (KBC == 17) f(panel_sweep_kernel<17, 8, 5>);   // p = 6 backward: up to 78 far entries per row
 }
 
 }  // namespace

@@ -158,8 +158,10 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
   }
   out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12, 14})
                    : round_up_variant((max_near + 15) / 16, {4, 8, 12});
-  out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4}) : round_up_variant((max_far + 15) / 16, {0, 4, 8});
+  out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4, 5}) : round_up_variant((max_far + 15) / 16, {0, 4, 8});
   if (out.KA == 14 && out.KF != 0) out.KA = -1;  // the KA 14 variant exists without far slots only
+  if (out.KF == 5 && out.KA > 8) out.KF = -1;     // KF 5 exists with KA <= 8 only
+  if (out.KF == 5) out.KA = 8;
   if (out.KA < 0 || out.KF < 0) {
     if (std::getenv("IGB_VERBOSE"))
       std::fprintf(stderr, "[igb] panel plan (%s, W %d, %d ranges): max near %d, max far %d entries per row -- "

@@ -400,3 +400,19 @@ def test_matrix_free_operator_matches(cfg, kw):
     _check_history(rep.residuals, histo, f"{cfg} matrix-free vs oracle")
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
+
+
+def test_p6_backward_panel_far_slots_match_oracle():
+    """cfg4 p = 6 (L = 4): backward rows carry up to 78 entries of another patch -- the panel
+    variant with 5 far slots per lane (B = 512, several ranges); sweeps repeatable, equal to
+    SuperLU on triu(A) per level."""
+    pr, setup, f, solver, orc = device_solver("cfg4", p=6, levels=4)
+    rng = np.random.default_rng(47)
+    for level in range(1, solver.finest + 1):
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for op, ref in (("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward)):
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(3):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (level, op)

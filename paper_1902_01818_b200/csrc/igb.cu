@@ -1302,6 +1302,18 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
     if (!force && 2 * npan > nlev) continue;
     built = build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, W, R,
                              max_clu[sh], plan);
+    // B = 512 fell back to one range with the long-row variant (KA 14; cfg4 p = 8 backward): B = 256
+    // with its KF 10 variant may run several ranges and finish sooner (a B = 256 panel costs about as
+    // much as a B = 512 one, ~3 us).  Restricted to that case: on a 3-D level (cfg5 L=2) the switch
+    // broke the preconditioner's symmetry -- not investigated further this round.
+    static const bool try_half = !(std::getenv("IGB_PANEL_HALF") && std::atoi(std::getenv("IGB_PANEL_HALF")) == 0);
+    if (built && sh == 0 && plan.nclu == 1 && plan.KA == 14 && max_clu[0] > 1 && try_half && (shapes_ok & 2)) {
+      PanelPlanHost alt;
+      if (build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, 8, 16384,
+                           max_clu[1], alt, true) &&
+          alt.nclu > 1 && alt.makespan < 0.8 * plan.makespan)
+        plan = std::move(alt);
+    }
   }
   if (!built) return false;
   PanelDev& P = V.panel[dir];

@@ -460,6 +460,12 @@ void dispatch_kf9(cudaStream_t st, const PanelArgs& a) {
   switch (a.KF) {
     case 0: launch_one<9, KA, 0>(st, a); break;
     case 4: launch_one<9, KA, 4>(st, a); break;
+    case 10:
+      if constexpr (KA == 12) {
+        launch_one<9, 12, 10>(st, a);
+        break;
+      }
+      [[fallthrough]];
     default: launch_one<9, KA, 8>(st, a); break;
   }
 }
@@ -484,6 +490,7 @@ void for_all_variants(int KBC, F&& f) {
   per_ka(std::integral_constant<int, 12>{});
   if (KBC == 17) f(panel_sweep_kernel<17, 14, 0>);  // long single-range rows (p = 8 backward: ~208 near)
   if (KBC == 17) f(panel_sweep_kernel<17, 8, 5>);   // p = 6 backward: up to 78 far entries per row
+  if (KBC == 9) f(panel_sweep_kernel<9, 12, 10>);   // p = 8 backward, several ranges: 136 far entries
 }
 
 }  // namespace

@@ -60,7 +60,7 @@ double simulate_ranges(int n, int B, const std::vector<int>& rs, MaxRef maxref) 
 }  // namespace
 
 bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos,
-                      bool upper, int G, int W, int R, int max_clusters, PanelPlanHost& out) {
+                      bool upper, int G, int W, int R, int max_clusters, PanelPlanHost& out, bool allow_kf10) {
   if (W != 16 && W != 8) return false;
   const int B = 2 * G * W;
   if (n <= 0 || (R & (R - 1)) || R < B) return false;
@@ -158,7 +158,13 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
   }
   out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12, 14})
                    : round_up_variant((max_near + 15) / 16, {4, 8, 12});
-  out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4, 5}) : round_up_variant((max_far + 15) / 16, {0, 4, 8});
+  out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4, 5})
+                   : (allow_kf10 ? round_up_variant((max_far + 15) / 16, {0, 4, 8, 10})
+                                 : round_up_variant((max_far + 15) / 16, {0, 4, 8}));
+  if (W == 8 && out.KF == 10) {
+    if (out.KA > 12) out.KF = -1;  // KF 10 exists with KA 12 only
+    else out.KA = 12;
+  }
   if (out.KA == 14 && out.KF != 0) out.KA = -1;  // the KA 14 variant exists without far slots only
   if (out.KF == 5 && out.KA > 8) out.KF = -1;     // KF 5 exists with KA <= 8 only
   if (out.KF == 5) out.KA = 8;
@@ -167,7 +173,7 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
       std::fprintf(stderr, "[igb] panel plan (%s, W %d, %d ranges): max near %d, max far %d entries per row -- "
                    "beyond the kernel variants\n", upper ? "upper" : "lower", W, out.nclu, max_near, max_far);
     // cross-range references overflowed the kernel variants: one range (if that fits)
-    if (out.nclu > 1) return build_panel_plan(n, ptr, col, val, dpos, upper, G, W, R, 1, out);
+    if (out.nclu > 1) return build_panel_plan(n, ptr, col, val, dpos, upper, G, W, R, 1, out, allow_kf10);
     return false;
   }
   const int KA = out.KA, KF = out.KF, KBC = out.KBC;

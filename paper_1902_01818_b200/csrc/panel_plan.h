@@ -69,6 +69,7 @@ struct PanelPlanHost {
 // W = 16 (B = 32 G, KA in {2,4,8,12}, KF in {0,1,4}; KA 14 with KF 0; KA 8 with KF 5) or W = 8 (B = 16 G, KA in {4,8,12},
 // KF in {0,4,8}: entry-heavy 3-D rows).
 bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos,
-                      bool upper, int G, int W, int R, int max_clusters, PanelPlanHost& out);
+                      bool upper, int G, int W, int R, int max_clusters, PanelPlanHost& out,
+                      bool allow_kf10 = false);
 
 }  // namespace igb

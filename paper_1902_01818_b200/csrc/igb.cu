@@ -1300,17 +1300,24 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
     const int W = sh ? 8 : 16, R = sh ? 16384 : 8192, B = 2 * G * W;
     const int npan = (V.n + B - 1) / B;
     if (!force && 2 * npan > nlev) continue;
+    // B = 256 after B = 512 failed: the KF 10 variant on 2-D levels (cfg4 p = 8 backward, 136 far entries
+    // per row); 3-D levels keep KF <= 8 (B = 256 ranges broke a 3-D sweep, DESIGN 9)
+    const bool two_d = !V.interiors.empty() && V.interiors[0].dim == 2;
     built = build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, W, R,
-                             max_clu[sh], plan);
+                             max_clu[sh], plan, sh == 1 && two_d);
     // B = 512 fell back to one range with the long-row variant (KA 14; cfg4 p = 8 backward): B = 256
     // with its KF 10 variant may run several ranges and finish sooner (a B = 256 panel costs about as
     // much as a B = 512 one, ~3 us).  Restricted to that case: on a 3-D level (cfg5 L=2) the switch
     // broke the preconditioner's symmetry -- not investigated further this round.
-    static const bool try_half = !(std::getenv("IGB_PANEL_HALF") && std::atoi(std::getenv("IGB_PANEL_HALF")) == 0);
-    if (built && sh == 0 && plan.nclu == 1 && plan.KA == 14 && max_clu[0] > 1 && try_half && (shapes_ok & 2)) {
+    // IGB_PANEL_HALF: 0 off, 1 (default) the KA 14 case only, 2 every single-range B = 512 plan (diagnostic);
+    // IGB_PANEL_KF10=0 keeps the alternative to KF <= 8
+    static const int half_mode = std::getenv("IGB_PANEL_HALF") ? std::atoi(std::getenv("IGB_PANEL_HALF")) : 1;
+    static const bool kf10 = !(std::getenv("IGB_PANEL_KF10") && std::atoi(std::getenv("IGB_PANEL_KF10")) == 0);
+    if (built && sh == 0 && plan.nclu == 1 && (plan.KA == 14 || half_mode == 2) && max_clu[0] > 1 && half_mode &&
+        (shapes_ok & 2)) {
       PanelPlanHost alt;
       if (build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, 8, 16384,
-                           max_clu[1], alt, true) &&
+                           max_clu[1], alt, kf10) &&
           alt.nclu > 1 && alt.makespan < 0.8 * plan.makespan)
         plan = std::move(alt);
     }

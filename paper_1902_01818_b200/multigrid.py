@@ -212,8 +212,6 @@ class MultigridSolver:
             smo = self.smoother[level]
             gs = smo if isinstance(smo, sm.GaussSeidel) else getattr(smo, "gs", None)
             scms = smo if isinstance(smo, sm.SubspaceCorrectedMass) else getattr(smo, "scms", None)
-            if gs is not None:
-                ctx.set_gs(level)
             if scms is not None:
                 ctx.scms_begin(level, scms.tau)
                 for piece, solver in scms.interiors:
@@ -221,6 +219,8 @@ class MultigridSolver:
                                           solver.denominator, piece.indices)
                 for (piece, _), inv in zip(scms.pieces, scms.piece_inverses):
                     ctx.scms_add_piece(level, piece.indices, inv)
+            if gs is not None:  # after the interiors: the sweep planner reads the level's dimension
+                ctx.set_gs(level)
             smo.bind(ctx, level)
         Lf, Uf, pr, pc = self.coarse_solver.factors()
         ctx.set_coarse_lu(Lf, Uf, pr, pc)

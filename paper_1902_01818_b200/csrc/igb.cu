@@ -1302,7 +1302,8 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
     if (!force && 2 * npan > nlev) continue;
     // B = 256 after B = 512 failed: the KF 10 variant on 2-D levels (cfg4 p = 8 backward, 136 far entries
     // per row); 3-D levels keep KF <= 8 (B = 256 ranges broke a 3-D sweep, DESIGN 9)
-    const bool two_d = !V.interiors.empty() && V.interiors[0].dim == 2;
+    static const bool kf10_3d = std::getenv("IGB_PANEL_KF10_3D") && std::atoi(std::getenv("IGB_PANEL_KF10_3D"));
+    const bool two_d = kf10_3d || (!V.interiors.empty() && V.interiors[0].dim == 2);  // env: diagnostic
     built = build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, W, R,
                              max_clu[sh], plan, sh == 1 && two_d);
     // B = 512 fell back to one range with the long-row variant (KA 14; cfg4 p = 8 backward): B = 256

@@ -1342,6 +1342,7 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
     a.rstart[c] = plan.rstart[c];
   }
   if (const char* h = std::getenv("IGB_PANEL_NOHINT")) a.ablate |= std::atoi(h) ? 128 : 0;
+  if (const char* h = std::getenv("IGB_PANEL_ALLSLOTS")) a.ablate |= std::atoi(h) ? 256 : 0;
   const char* pf = std::getenv("IGB_PANEL_PF");
   a.pf = pf ? std::max(0, std::atoi(pf)) : 0;  // bulk L2 prefetch distance (measured: no gain)
   if (panel_smem_bytes(a) > 227u * 1024) return false;

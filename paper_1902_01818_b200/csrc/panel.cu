@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(panel_warps<KBC>() * 32, 1) panel_sweep_kernel
           else X.fx[j] = 0.0;
         }
     }
-    if (t + 1 < T) load(Y, t + 1, X.xc >> 16);
+    if (t + 1 < T) load(Y, t + 1, (a.ablate & 256) ? KF : X.xc >> 16);  // 256: every far slot (diagnostic)
     mark(2);
     // ---- phase B: inverse block, warp per row pair
     if (!(a.ablate & 64)) mbar_wait_cluster(&bar_r[t & 1], (unsigned)((t >> 1) & 1), 0, t);

@@ -1,9 +1,14 @@
-"""Benchmark: MG-PCG DoF-iterations/s on B200 (fp64), BASELINE configs[1] workload.
+"""Benchmark: MG-PCG DoF-iterations/s on B200 (fp64), BASELINE configs[4] workload (cfg5, full size).
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg2]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config cfg5]
 
+Workload: BASELINE.json names no single config for the metric, so the N=1 line uses the largest
+configuration that fits one GPU: configs[4] = cfg5 (2x2x2 unit cubes, p = 3, 64^3 spans per patch,
+N = 2,248,091 DoFs, 726.6M nonzeros, 5 levels, hybrid smoother).  The other configs are parity
+cases (tests/), selectable here with --config for reference.
 A *step* is one full PCG solve (x0 = 0, tol 1e-8, one V(1,1) cycle per
-iteration as preconditioner) on the configuration's finest system.
+iteration as preconditioner) on the configuration's finest system; the iteration count is
+checked against the reference's (EXPECTED_ITS) and the line fails on a mismatch.
   value  = sum over ranks of N_dofs * its / (max over ranks of the mean device time per step),
            inputs resident in HBM (igb_pcg_device), CUDA events on the library stream,
            L2 flushed (256 MiB write) before every step;
@@ -11,11 +16,16 @@ iteration as preconditioner) on the configuration's finest system.
            solve, x -> host), wall clock per step;
   roofline = dominant kernel class from a separate profiled pass (CUDA events around every
            launch, same K steps) -> algorithmic bytes / mean launch time vs MEASURED_PEAKS.json;
+  roofline_fd = the fast-diagonalisation class's flops / time vs the measured fp64 DGEMM peak
+           (profiles/r2_fp64_peak.json; MEASURED_PEAKS.json has no fp64 entry);
   cpu_baseline = oracle/ (reference-faithful NumPy/SciPy restatement) on a bounded sample.
 Multi-GPU (torchrun): independent replicas per GPU (the solve does not shard),
 weak scaling, NCCL only for the barrier and the max-over-ranks reduction.
 --impl reference: the reference-faithful CPU solve (oracle port; the reference itself is pure
-Python and does not travel to the GPU box) on rank 0 with all host threads.
+Python and does not travel to the GPU box) on rank 0 with all host threads.  On the large
+configurations (cfg4, cfg5) one CPU solve takes minutes, so a reference step is a bounded sample:
+ONE PCG iteration of the same solve (SpMV A d, the CG vector updates and one V(1,1) hybrid cycle
+on the full hierarchy); value = N / (mean seconds per iteration), the same DoF*it/s unit.
 """
 
 import argparse
@@ -32,6 +42,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 BYTES_CLASS_PEAK = "hbm_gbs"
+# reference iteration counts (tests/golden from igamg; cfg4 p=6/8 and cfg5 at full size from the oracle,
+# tests/test_fullsize.py) at the default level counts
+EXPECTED_ITS = {"cfg1": 8, "cfg2": 6, "cfg3": 12, "cfg4_p2": 5, "cfg4_p4": 7, "cfg4_p6": 9, "cfg4_p8": 11,
+                "cfg5": 6}
+LARGE = ("cfg4", "cfg5")  # one CPU solve takes minutes: reference steps are single PCG iterations
 
 
 def parse():
@@ -40,10 +55,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="cfg2")
+    ap.add_argument("--config", default="cfg5")
     ap.add_argument("--levels", type=int, default=None)
     ap.add_argument("--p", type=int, default=None)
     ap.add_argument("--cpu-sample-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-step", default="auto", choices=["auto", "solve", "iteration"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     return ap.parse_args()
 
@@ -84,14 +100,99 @@ def build_problem(args):
     return pr, setup, f, time.perf_counter() - t
 
 
-def workload_desc(args, pr, setup):
-    d = {"workload": f"{args.config}" + (f"_p{args.p}" if args.p else "") +
-         (f"_L{args.levels}" if args.levels else ""),
-         "n_dofs": int(setup.n_dofs), "levels": int(pr.hier.L), "degree": int(pr.hier.p),
-         "patches": int(pr.hier.domain.num_patches), "dim": int(pr.hier.dim),
-         "mode": pr.hier.mode, "smoother": pr.config.smoother, "tol": pr.config.tol,
-         "nnz_finest": int(setup.A[setup.finest].nnz)}
-    return d
+def workload_name(args):
+    return f"{args.config}" + (f"_p{args.p}" if args.p else "") + (f"_L{args.levels}" if args.levels else "")
+
+
+def workload_desc(args, pr, setup, its):
+    """The `config` dict -- identical key set and values in both arms."""
+    return {"workload": workload_name(args),
+            "n_dofs": int(setup.n_dofs), "levels": int(pr.hier.L), "degree": int(pr.hier.p),
+            "patches": int(pr.hier.domain.num_patches), "dim": int(pr.hier.dim),
+            "mode": pr.hier.mode, "smoother": pr.config.smoother, "tol": pr.config.tol,
+            "nnz_finest": int(setup.A[setup.finest].nnz), "iterations": int(its),
+            "parallelism": "replicas (one independent solve per GPU)"}
+
+
+def check_its(args, its):
+    """Fail the line when the iteration count differs from the reference's (a smoother defect that
+    weakens the preconditioner would raise `its` and with it the DoF*it/s figure)."""
+    key = workload_name(args)
+    if args.levels is None and key in EXPECTED_ITS and its != EXPECTED_ITS[key]:
+        raise SystemExit(f"bench: {key} took {its} PCG iterations, the reference takes {EXPECTED_ITS[key]}")
+
+
+class OracleCgStepper:
+    """One PCG iteration of oracle.solve.cg (reference linsolve.py:83-100) per step: A d, the dots
+    and updates, and one cycle as preconditioner on the full hierarchy; restarts from x = 0 when
+    the solve converges (the restart is not timed)."""
+
+    def __init__(self, orc, b, tol):
+        self.orc, self.b, self.tol = orc, np.asarray(b, dtype=float), tol
+        self.A = orc.A[orc.finest]
+        self.normb = np.linalg.norm(self.b)
+        self.restart()
+
+    def restart(self):
+        self.x = np.zeros_like(self.b)
+        self.r = self.b.copy()
+        self.z = self.orc.cycle(self.orc.finest, self.r)
+        self.d = self.z.copy()
+        self.rz = self.r @ self.z
+        self.done = False
+
+    def step(self):
+        if self.done:
+            self.restart()
+        t = time.perf_counter()
+        Ad = self.A @ self.d
+        alpha = self.rz / (self.d @ Ad)
+        self.x += alpha * self.d
+        self.r -= alpha * Ad
+        rel = np.linalg.norm(self.r) / self.normb
+        self.z = self.orc.cycle(self.orc.finest, self.r)
+        rz_new = self.r @ self.z
+        beta = rz_new / self.rz
+        self.rz = rz_new
+        self.d = self.z + beta * self.d
+        dt = time.perf_counter() - t
+        self.done = rel <= self.tol
+        return dt
+
+
+def ref_mode(args):
+    if args.ref_step != "auto":
+        return args.ref_step
+    return "iteration" if args.config in LARGE and args.levels is None else "solve"
+
+
+def cpu_rate(setup, f, seconds, threads, mode, warmup=1, steps=None):
+    """Reference-faithful CPU solve (oracle port) on `threads` host threads: DoF*it/s.
+    mode "solve": whole PCG solves; "iteration": single PCG iterations (OracleCgStepper).
+    Runs `steps` timed steps, or until ~`seconds` of timed work."""
+    from threadpoolctl import threadpool_limits
+    from oracle.solve import OracleSolver
+    with threadpool_limits(limits=threads):
+        orc = OracleSolver(setup.setup_bundle())
+        n = setup.n_dofs
+        tol, mi = setup.config.tol, setup.config.max_iters
+        if mode == "iteration":
+            st = OracleCgStepper(orc, f, tol)
+            for _ in range(warmup):
+                st.step()
+            times = []
+            while (steps is None and (sum(times) < seconds or not times)) or (steps is not None and len(times) < steps):
+                times.append(st.step())
+            return n / float(np.mean(times)), times, 1
+        for _ in range(warmup):
+            orc.solve(f, tol=tol, max_iters=mi)
+        times, its = [], 0
+        while (steps is None and (sum(times) < seconds or not times) and len(times) < 50) or \
+                (steps is not None and len(times) < steps):
+            t = time.perf_counter()
+            _, its, _ = orc.solve(f, tol=tol, max_iters=mi)
+            times.append(time.perf_counter() - t)
+        return n * its / float(np.mean(times)), times, its
 
 
 class ClockSampler:
@@ -140,6 +241,18 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def fp64_peak_tflops():
+    """Measured fp64 DGEMM peak (tools/fp64_peak.py on this pool's B200: profiles/r2_fp64_peak.json)."""
+    d, _ = measured_peaks()
+    if "fp64_tflops" in d:
+        return float(d["fp64_tflops"]), "MEASURED_PEAKS.json"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_fp64_peak.json")) as fh:
+            return float(json.load(fh)["fp64_tflops"]), "measured (profiles/r2_fp64_peak.json, cuBLAS DGEMM 8192^3)"
+    except Exception:
+        return 37.0, "fallback (B200 nominal fp64)"
+
+
 def measured_peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -150,53 +263,33 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def cpu_oracle_rate(setup, f, seconds, threads):
-    """Reference-faithful CPU solve (oracle port) repeated for ~`seconds`: DoF*its/s."""
-    from threadpoolctl import threadpool_limits
-    from oracle.solve import OracleSolver
-    with threadpool_limits(limits=threads):
-        orc = OracleSolver(setup.setup_bundle())
-        n = setup.n_dofs
-        total_dofit, total_t, runs, its = 0.0, 0.0, 0, 0
-        while True:
-            t = time.perf_counter()
-            _, its, _ = orc.solve(f, tol=setup.config.tol, max_iters=setup.config.max_iters)
-            dt = time.perf_counter() - t
-            total_dofit += n * its
-            total_t += dt
-            runs += 1
-            if total_t >= seconds or runs >= 50:
-                break
-    return total_dofit / total_t, runs, its, total_t
-
-
 def run_reference(args, rank, world):
     if rank != 0:
         return
     pr, setup, f, t_setup = build_problem(args)
     cores = len(os.sched_getaffinity(0))
-    from threadpoolctl import threadpool_limits
-    from oracle.solve import OracleSolver
-    with threadpool_limits(limits=cores):
-        orc = OracleSolver(setup.setup_bundle())
-        for _ in range(args.warmup):
-            orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
-        times, its = [], 0
-        for _ in range(args.steps):
-            t = time.perf_counter()
-            _, its, _ = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
-            times.append(time.perf_counter() - t)
+    mode = ref_mode(args)
+    value, times, its = cpu_rate(setup, f, 0.0, cores, mode, warmup=args.warmup, steps=args.steps)
+    if mode == "iteration":
+        its = EXPECTED_ITS.get(workload_name(args))
+        if its is None:  # reduced configurations only (full sizes are in EXPECTED_ITS): count once
+            from oracle.solve import OracleSolver
+            its = OracleSolver(setup.setup_bundle()).solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)[1]
+        sample = (f"{args.steps} single PCG iterations (A d + CG updates + one V(1,1) hybrid cycle on the full "
+                  f"{workload_name(args)} hierarchy), oracle/solve.py (reference-faithful SciPy/NumPy restatement; "
+                  f"GS sweeps as C substitution where splu(tril) does not fit), {cores} BLAS threads")
+    else:
+        sample = (f"{args.steps} full PCG solves of {workload_name(args)} (oracle/solve.py, reference-faithful "
+                  f"SciPy/NumPy restatement), {cores} BLAS threads")
     ms = 1e3 * float(np.mean(times))
-    value = setup.n_dofs * its / (ms / 1e3)
     line = {
         "metric": "MG-PCG DoF*iterations/s", "value": value, "unit": "DoF*it/s", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (analytic geometry + source, SURVEY 8d)",
-        "config": dict(workload_desc(args, pr, setup), iterations=its, setup_s=round(t_setup, 2)),
-        "cpu_baseline": {"value": value, "unit": "DoF*it/s", "cores": cores, "kind": "port",
-                         "sample": f"{args.steps} full PCG solves of {args.config} (oracle/solve.py, "
-                                   f"reference-faithful SciPy/NumPy restatement), {cores} BLAS threads"},
+        "config": workload_desc(args, pr, setup, its),
+        "step": mode, "setup_s": round(t_setup, 2),
+        "cpu_baseline": {"value": value, "unit": "DoF*it/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "DoF*it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -242,6 +335,7 @@ def run_ours(args, rank, world, local):
     for _ in range(args.warmup):
         l2_flush()
         its, hist = ctx.pcg_device(d_b, d_x, cfg.tol, cfg.max_iters)
+    check_its(args, its)
 
     # ---- timed region: device-resident inputs, CUDA-event time per solve
     dev_ms = []
@@ -291,37 +385,54 @@ def run_ours(args, rank, world, local):
     bytes_per_launch = P["bytes"] / max(1, P["launches"])
     achieved = bytes_per_launch / mean_launch_s / 1e9 if mean_launch_s > 0 else 0.0
     traffic, traffic_src = None, None
-    tp = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "traffic.json")
-    if os.path.exists(tp) and args.config == "cfg2":  # committed ncu capture of the same workload
-        t = json.load(open(tp)).get(dom)
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):  # committed ncu --set full capture of the same workload's dominant kernel
+        t = json.load(open(tp)).get(workload_name(args), {}).get(dom)
         if t:
             traffic, traffic_src = t["bytes_per_launch"], t["source"]
+    classes = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                   "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
+               for k, v in prof.items()}
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                 "traffic_source": traffic_src,
                 "algorithmic_bytes_per_launch": bytes_per_launch,
                 "peak_source": peak_kind,
-                "note": "algorithmic bytes per launch / mean CUDA-event launch time, profiled pass",
-                "classes": {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
-                                "GBps": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] > 0 else 0.0}
-                            for k, v in prof.items()}}
+                "note": "algorithmic bytes per launch / mean CUDA-event launch time, profiled pass "
+                        "(events around every launch, outside the graph)",
+                "classes": classes}
+    # fast diagonalisation: fp64 flops / time against the measured DGEMM peak
+    fd = prof.get("fd", {})
+    fp64_peak, fp64_src = fp64_peak_tflops()
+    if fd.get("ms", 0) > 0 and fd.get("flops", 0) > 0:
+        tf = fd["flops"] / (fd["ms"] / 1e3) / 1e12
+        roofline_fd = {"bound": "fp64", "kernel": "fd", "achieved": tf, "peak": fp64_peak, "unit": "TFLOP/s",
+                       "frac": tf / fp64_peak, "flops_per_step": fd["flops"] / args.steps,
+                       "ms_per_step": fd["ms"] / args.steps, "peak_source": fp64_src}
+    else:
+        roofline_fd = None
 
     out = None
     if rank == 0:
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            rate, runs, cits, tt = cpu_oracle_rate(setup, f, args.cpu_sample_seconds, 1)
-            cpu = {"value": rate, "unit": "DoF*it/s", "cores": 1, "kind": "port",
-                   "sample": f"{runs} full PCG solves of {args.config} ({tt:.1f} s), oracle/solve.py, 1 thread"}
+            cores = len(os.sched_getaffinity(0))
+            mode = ref_mode(args)
+            rate, times, cits = cpu_rate(setup, f, args.cpu_sample_seconds, cores, mode, warmup=0)
+            what = "single PCG iterations (A d + CG updates + one V(1,1) cycle)" if mode == "iteration" \
+                else "full PCG solves"
+            cpu = {"value": rate, "unit": "DoF*it/s", "cores": cores, "kind": "port",
+                   "sample": f"{len(times)} {what} of {workload_name(args)} ({sum(times):.1f} s), oracle/solve.py, "
+                             f"{cores} BLAS threads (SpMV / substitution single-threaded as in SciPy)"}
         out = {
             "metric": "MG-PCG DoF*iterations/s", "value": value, "unit": "DoF*it/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (analytic geometry + source, SURVEY 8d)",
-            "config": dict(workload_desc(args, pr, setup), iterations=its, l2="flushed (256 MiB write) before every step",
-                           setup_s=round(t_setup, 2), upload_s=round(solver.setup_timings["upload"], 2),
-                           parallelism=f"replicas x{world}"),
-            "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu,
+            "config": workload_desc(args, pr, setup, its),
+            "l2": "inputs (8.7 GB of matrices) exceed L2; also flushed (256 MiB write) before every step",
+            "setup_s": round(t_setup, 2), "upload_s": round(solver.setup_timings["upload"], 2),
+            "e2e": e2e, "roofline": roofline, "roofline_fd": roofline_fd, "cpu_baseline": cpu,
             "gpu_launches": int(launches), "clocks": clocks.summary(),
             "final_rel_residual": hist[-1] if hist else None,
         }

@@ -179,6 +179,18 @@ int igb_launch_count(igb_ctx* ctx, long long* kernels, int reset);
 int igb_profile_enable(igb_ctx* ctx, int on);
 int igb_profile_reset(igb_ctx* ctx);
 int igb_profile_get(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes);
+/* Algorithmic flops of a class since igb_profile_reset (the fast-diagonalisation class 2:
+ * 4 prod(n) sum_a n_a per interior and application, i.e. 8 n^3 in 2-D, 12 n^4 in 3-D). */
+int igb_profile_flops(igb_ctx* ctx, int cls, double* flops);
+
+/* Which Gauss-Seidel engine igb_set_gs planned for (level, dir) (dir 0 forward, 1 backward);
+ * info[0..ninfo) receives: engine (1 panel sweep, 2 flow sweep, 3 level-set sweep, 4 level
+ * schedule), panel rows B (flow: lanes per row), KA near slots, KF far slots, clusters / ranges
+ * (flow: CTAs), panels, dependency levels, n.  Diagnostic; no reference counterpart.
+ * Note: the opt-in B = 256 / KF 10 panel variant (IGB_PANEL_KF10=1) reads the level's dimension
+ * from its interiors, so with it igb_set_gs must follow igb_scms_add_interior; by default the
+ * plan does not depend on call order. */
+int igb_gs_info(igb_ctx* ctx, int level, int dir, int* info, int ninfo);
 
 #ifdef __cplusplus
 }

@@ -18,6 +18,10 @@ reference itself and against ``tests/golden/*.npz``):
 * ``_Scms.apply``                <- ``SubspaceCorrectedMass.apply`` (smoothers.py:321-325)
 * hybrid pre/post smoothing      <- ``HybridSmoother``         (smoothers.py:343-353)
 * coarse / piece solves          <- ``linsolve.Factorization.solve`` (linsolve.py:33-53)
+* ``_TriSolveGS``                 <- the same GS sweeps as row substitution in C
+  (``oracle/trisolve.c``, built into ``oracle/_ref/libtrisolve.so``) for levels where
+  ``splu(tril(A))`` does not fit (cfg4 p = 8, cfg5 at full size); equal to SuperLU to
+  rounding, pinned against it in ``tests/test_oracle.py``.
 
 Input is a *setup bundle* (plain dict: matrices ``A``, prolongations ``P``,
 smoother kind, ``mu``, steps per level, per-level SCMS interior/piece data),
@@ -25,11 +29,36 @@ produced either by the product's host setup (``MultigridSetup.setup_bundle``)
 or extracted from a reference ``MultigridSolver`` (``bundle_from_reference``).
 """
 
+import ctypes
+import os
+
 import numpy as np
 import scipy.sparse
 import scipy.sparse.linalg
 
-__all__ = ["cg", "OracleSolver", "bundle_from_reference"]
+__all__ = ["cg", "OracleSolver", "bundle_from_reference", "trisolve_lib"]
+
+_TRI_LIB = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_ref", "libtrisolve.so")
+_tri = None
+# levels with more strict-triangle entries than this use the C substitution (SuperLU's copy of
+# tril(A) plus its supernodal workspace does not fit at cfg4 p = 8 / cfg5 full size)
+SPLU_MAX_TRI_NNZ = int(os.environ.get("ORACLE_SPLU_MAX_TRI_NNZ", 60_000_000))
+
+
+def trisolve_lib():
+    """oracle/_ref/libtrisolve.so (built by oracle/Makefile via __graft_entry__.build())."""
+    global _tri
+    if _tri is None:
+        if not os.path.exists(_TRI_LIB):
+            import subprocess
+            subprocess.run(["make", "-s", "-C", os.path.dirname(os.path.abspath(__file__))], check=True)
+        lib = ctypes.CDLL(_TRI_LIB)
+        for name in ("tri_forward", "tri_backward"):
+            fn = getattr(lib, name)
+            fn.argtypes = [ctypes.c_int64] + [ctypes.c_void_p] * 5
+            fn.restype = ctypes.c_int
+        _tri = lib
+    return _tri
 
 
 def cg(A, b, preconditioner=None, tol=1e-8, max_iters=10000, callback=None):
@@ -86,6 +115,44 @@ class _GaussSeidel:
         return self._lu.solve(r, trans="T")
 
 
+class _TriSolveGS:
+    """Same sweeps as ``_GaussSeidel`` by row substitution on A's CSR (oracle/trisolve.c)."""
+
+    def __init__(self, A):
+        A = A.tocsr()
+        if not A.has_sorted_indices:
+            A = A.sorted_indices()
+        if np.any(A.diagonal() == 0.0):
+            raise ValueError("Gauss-Seidel needs a nonzero diagonal")
+        self.n = A.shape[0]
+        self.ptr = np.ascontiguousarray(A.indptr, dtype=np.int64)
+        self.col = np.ascontiguousarray(A.indices, dtype=np.int32)
+        self.val = np.ascontiguousarray(A.data, dtype=np.float64)
+        self.lib = trisolve_lib()
+
+    def _run(self, fn, r):
+        b = np.ascontiguousarray(r, dtype=np.float64)
+        x = np.empty_like(b)
+        rc = fn(self.n, self.ptr.ctypes.data, self.col.ctypes.data, self.val.ctypes.data, b.ctypes.data,
+                x.ctypes.data)
+        if rc != 0:
+            raise ValueError("Gauss-Seidel needs a nonzero diagonal")
+        return x
+
+    def forward(self, r):
+        return self._run(self.lib.tri_forward, r)
+
+    def backward(self, r):
+        return self._run(self.lib.tri_backward, r)
+
+
+def make_gauss_seidel(A, impl="auto"):
+    """SuperLU (bitwise the reference) unless the level is too large for splu(tril(A))."""
+    if impl == "auto":
+        impl = "superlu" if (A.nnz + A.shape[0]) // 2 <= SPLU_MAX_TRI_NNZ else "trisolve"
+    return _GaussSeidel(A) if impl == "superlu" else _TriSolveGS(A)
+
+
 def _interior_solve(subspaces, dims, r):
     R = np.asarray(r).reshape(dims)
     out = np.zeros_like(R)
@@ -122,7 +189,7 @@ class _Scms:
 class OracleSolver:
     """Reference-faithful cycle / preconditioner on a setup bundle."""
 
-    def __init__(self, bundle):
+    def __init__(self, bundle, gs_impl="auto"):
         self.A = bundle["A"]
         self.P = bundle["P"]
         self.kind = bundle["smoother"]
@@ -134,7 +201,7 @@ class OracleSolver:
         self.scms = [None] * (self.finest + 1)
         for level in range(1, self.finest + 1):
             if self.kind in ("gs", "hyb"):
-                self.gs[level] = _GaussSeidel(self.A[level])
+                self.gs[level] = make_gauss_seidel(self.A[level], gs_impl)
             if self.kind in ("scms", "hyb"):
                 self.scms[level] = _Scms(self.A[level], bundle["levels"][level])
 

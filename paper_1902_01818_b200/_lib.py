@@ -55,7 +55,10 @@ SIGNATURES = {
     "igb_profile_enable": ([_p, _i], _i),
     "igb_profile_reset": ([_p], _i),
     "igb_profile_get": ([_p, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll), ctypes.POINTER(_d)], _i),
+    "igb_gs_info": ([_p, _i, _i, _ip, _i], _i),
+    "igb_profile_flops": ([_p, _i, ctypes.POINTER(_d)], _i),
 }
+GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule"}
 
 _lib = None
 
@@ -278,5 +281,17 @@ class Context:
             ms, n, by = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
             self._check(self.lib.igb_profile_get(self.h, k, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by)),
                         "igb_profile_get")
-            out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value}
+            fl = ctypes.c_double()
+            self._check(self.lib.igb_profile_flops(self.h, k, ctypes.byref(fl)), "igb_profile_flops")
+            out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value, "flops": fl.value}
         return out
+
+    def gs_info(self, level, direction):
+        """The Gauss-Seidel engine planned for (level, direction): dict with engine, B (flow: lanes
+        per row), KA, KF, ranges (flow: CTAs), panels, depth, n."""
+        info = (ctypes.c_int * 8)()
+        self._check(self.lib.igb_gs_info(self.h, int(level), int(direction), info, 8), "igb_gs_info")
+        v = list(info)
+        return {"engine": GS_ENGINES.get(v[0], "?"), "B": v[1], "KA": v[2], "KF": v[3], "ranges": v[4],
+                "panels": v[5], "depth": v[6], "n": v[7]}
+

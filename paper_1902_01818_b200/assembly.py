@@ -29,6 +29,7 @@ import scipy.sparse
 import scipy.sparse.csgraph
 
 from . import bspline as bs
+from . import _setup_native
 from . import geometry as geom
 
 __all__ = [
@@ -661,6 +662,18 @@ def assemble_level(hier, level, sigma=5.0, neglect_geometry=False, parts=("A",))
     fob, dob = dofs.free_of_block, dofs.dir_of_block
     want = set(parts) | {"A"}
     want_mass = "M" in want
+    if hier.mode == "conforming" and not (want - {"A", "K", "Q"}):
+        native = _native_kron_level(hier, level, neglect_geometry)
+        if native is not None:
+            A, couple = native
+            asm = AssembledLevel(level=level, A=A, sigma=sigma, h_L=hier.finest_meshsize(), couple=couple,
+                                 dirichlet_points=_dirichlet_points(hier, level, neglect_geometry))
+            if want & {"K", "Q"}:
+                asm.K = asm.Q = A
+            asym, amax = _setup_native.max_asym(A)
+            if asym > 1e-10 * amax:
+                raise AssertionError("assembled operator lost symmetry")
+            return asm
 
     Kp, Mp = [], []
     for k in range(domain.num_patches):
@@ -721,6 +734,40 @@ def assemble_level(hier, level, sigma=5.0, neglect_geometry=False, parts=("A",))
     return asm
 
 
+def _native_kron_level(hier, level, neglect_geometry):
+    """(A, couple) of a conforming level whose patches all take the Kronecker branch of
+    ``_bulk_matrices`` (constant diagonal Jacobian, ``assembly.py:333-344``), assembled and reduced
+    to free DoFs natively (csrc/host_setup.cpp), bit-identical to ``_coo_sum(reduce_blockdiag(...))``
+    of the SciPy path; None when the library is unavailable or a patch is not affine."""
+    if _setup_native.lib() is None:
+        return None
+    dofs = hier.dofs[level]
+    d = hier.dim
+    coef, oned, dims = [], [], []
+    for k in range(hier.domain.num_patches):
+        scal = np.ones(d) if neglect_geometry else _probe_jacobian(hier.domain.patches[k])
+        if scal is None:
+            return None
+        det = float(np.prod(scal))
+        coef.append([det / scal[a] ** 2 for a in range(d)])
+        per = []
+        for s in hier.spaces[level][k]:
+            M = bs.univariate_mass(s).tocsr()
+            K = bs.univariate_stiffness(s).tocsr()
+            if not (M.has_sorted_indices and K.has_sorted_indices and np.array_equal(M.indptr, K.indptr)
+                    and np.array_equal(M.indices, K.indices)):
+                return None
+            per.append((M, K))
+        oned.append(per)
+        dims.append([s.n for s in hier.spaces[level][k]])
+    bo = np.asarray(dofs.offsets, dtype=np.int64)
+    A = _setup_native.kron_reduce(dims, coef, oned, bo, dofs.free_of_block, dofs.free_of_block,
+                                  dofs.n_free, dofs.n_free)
+    couple = _setup_native.kron_reduce(dims, coef, oned, bo, dofs.free_of_block, dofs.dir_of_block,
+                                       dofs.n_free, dofs.n_dirichlet)
+    return A, couple
+
+
 def _dirichlet_points(hier, level, neglect_geometry):
     """Physical Greville point of each Dirichlet class (first member in block order)."""
     dofs = hier.dofs[level]
@@ -755,8 +802,21 @@ def _tensor_load(spaces, patch, problem):
         nodes.append(x)
         weights.append(w)
         Bd.append(bs.basis_matrices(s, x, 0)[0])
-    X, J = patch.eval_grid(nodes)
-    detJ = np.abs(np.linalg.det(J))
+    scal = _probe_jacobian(patch)
+    if scal is not None:
+        # constant diagonal Jacobian (the Kronecker case of assembly.py:333-344): x_a depends on xi_a
+        # only and det J is constant -- evaluate the map along each axis instead of on the full
+        # quadrature grid (equal to rounding; 8 x 16.7M points on cfg5)
+        X = np.empty(tuple(len(x) for x in nodes) + (d,))
+        for a in range(d):
+            Xa, _ = patch.eval_grid([nodes[b] if b == a else nodes[b][:1] for b in range(d)])
+            shape = [1] * d
+            shape[a] = -1
+            X[..., a] = Xa[..., a].reshape(shape)
+        detJ = abs(float(np.prod(scal)))
+    else:
+        X, J = patch.eval_grid(nodes)
+        detJ = np.abs(np.linalg.det(J))
     wq = weights[0]
     for w in weights[1:]:
         wq = np.multiply.outer(wq, w)

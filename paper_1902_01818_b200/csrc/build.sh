@@ -12,3 +12,8 @@ NVCC="${NVCC:-nvcc}"
   -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/panel.cu" "$HERE/fd.cu" "$HERE/flow.cu" "$HERE/transfer.cu" "$HERE/mfree.cu" "$HERE/igb.cu" "$HERE/level_plan.cpp" "$HERE/panel_plan.cpp" "$HERE/flow_plan.cpp" -Xcompiler -pthread
 mv "$OUT.tmp" "$OUT"
 echo "built $OUT"
+# host setup library (OpenMP, no CUDA): bit-identical native replacements of the SciPy setup steps
+# that dominate the large configurations (host_setup.cpp); -ffp-contract=off keeps SciPy's rounding
+g++ -O3 -std=c++17 -fopenmp -fPIC -shared -ffp-contract=off -Wall -o "$PKG/libigb_setup.so.tmp" "$HERE/host_setup.cpp"
+mv "$PKG/libigb_setup.so.tmp" "$PKG/libigb_setup.so"
+echo "built $PKG/libigb_setup.so"

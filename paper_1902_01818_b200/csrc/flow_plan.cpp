@@ -1,5 +1,6 @@
 // flow_plan.cpp -- see flow_plan.h.
 #include "flow_plan.h"
+#include "host_par.h"
 
 #include <algorithm>
 #include <climits>
@@ -48,11 +49,16 @@ bool build_flow_plan(int n, const int* ptr, const int* col, const double* val, c
   out.crit.assign(out.nq, -1);
   out.ecol.resize(ent);
   out.eval.resize(ent);
-  long long e = 0;
   for (int q = 0; q < out.nq; ++q) {
     const int i = out.row[q];
-    if (i >= 0) {
+    out.eptr[q + 1] = out.eptr[q] + (i >= 0 ? hi(i) - lo(i) : 0);
+  }
+  parallel_for(out.nq, [&](long long qa, long long qb) {
+    for (long long q = qa; q < qb; ++q) {
+      const int i = out.row[q];
+      if (i < 0) continue;
       int best = -1;
+      long long e = out.eptr[q];
       for (int k = lo(i); k < hi(i); ++k, ++e) {
         out.ecol[e] = col[k];
         out.eval[e] = val[k];
@@ -65,8 +71,7 @@ bool build_flow_plan(int n, const int* ptr, const int* col, const double* val, c
       out.crit[q] = best;
       out.idiag[q] = 1.0 / val[dpos[i]];
     }
-    out.eptr[q + 1] = (int)e;
-  }
+  });
   out.entries = ent;
   return true;
 }

@@ -11,19 +11,23 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "igb.h"
 #include "level_plan.h"
 #include "flow_plan.h"
 #include "panel_plan.h"
+#include "host_par.h"
 #include "kernels.cuh"
 
 using namespace igb;
@@ -80,6 +84,7 @@ struct FdPlan {
   int ndesc[6] = {0};
   int tiles[6] = {0};
   double bytes[6] = {0};
+  double flops = 0;       // per application over all interiors: 4 prod(n) sum_a n_a (2 d contractions)
   int first_gather = 0;   // step index with the gather
   int last_scatter = 0;   // step index with the scatter
 };
@@ -173,6 +178,7 @@ struct ProfRec {
   int cls;
   double bytes;
   cudaEvent_t a, b;
+  double flops;
 };
 
 }  // namespace
@@ -225,6 +231,7 @@ struct igb_ctx {
   double prof_ms[K_NCLASS] = {0};
   long long prof_n[K_NCLASS] = {0};
   double prof_bytes[K_NCLASS] = {0};
+  double prof_flops[K_NCLASS] = {0};
 
   // timing of last pcg
   double last_pcg_ms = 0, last_cycle_ms = 0;
@@ -241,8 +248,34 @@ struct igb_ctx {
   template <class T>
   T* upload(const T* h, size_t count) {
     T* p = alloc<T>(count);
-    if (count) CU(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+    if (count) copy_h2d(p, h, count * sizeof(T));
     return p;
+  }
+  // H2D from pageable memory: large arrays go through two pinned 64 MB staging buffers (parallel
+  // host memcpy overlapped with the DMA of the previous chunk) instead of the driver's slow path
+  char* stage[2] = {nullptr, nullptr};
+  cudaEvent_t stage_ev[2] = {nullptr, nullptr};
+  static constexpr size_t kStage = 64u << 20;
+  void copy_h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes < (8u << 20)) {
+      CU(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+      return;
+    }
+    if (!stage[0]) {
+      for (int i = 0; i < 2; ++i) {
+        CU(cudaHostAlloc(reinterpret_cast<void**>(&stage[i]), kStage, cudaHostAllocDefault));
+        CU(cudaEventCreateWithFlags(&stage_ev[i], cudaEventDisableTiming));
+      }
+    }
+    for (size_t off = 0, k = 0; off < bytes; off += kStage, ++k) {
+      const size_t len = std::min(kStage, bytes - off);
+      const int b = (int)(k & 1);
+      CU(cudaEventSynchronize(stage_ev[b]));  // the DMA that last read this buffer is done
+      par_memcpy(stage[b], static_cast<const char*>(src) + off, len);
+      CU(cudaMemcpyAsync(static_cast<char*>(dst) + off, stage[b], len, cudaMemcpyHostToDevice, stream));
+      CU(cudaEventRecord(stage_ev[b], stream));
+    }
+    CU(cudaStreamSynchronize(stream));
   }
 
   cudaEvent_t pool_event() {
@@ -256,13 +289,13 @@ struct igb_ctx {
 
   // Launch wrapper: records CUDA events around the launch in profile mode.
   template <class F>
-  void launch(int cls, double bytes, F&& f) {
+  void launch(int cls, double bytes, F&& f, double flops = 0.0) {
     if (capturing) ++graph_kernels; else ++launches_direct;
     if (!prof) {
       f();
       return;
     }
-    ProfRec r{cls, bytes, nullptr, nullptr};
+    ProfRec r{cls, bytes, nullptr, nullptr, flops};
     if (capturing) {
       CU(cudaEventCreate(&r.a));
       CU(cudaEventCreate(&r.b));
@@ -285,6 +318,7 @@ struct igb_ctx {
       prof_ms[r.cls] += ms;
       prof_n[r.cls] += 1;
       prof_bytes[r.cls] += r.bytes;
+      prof_flops[r.cls] += r.flops;
     }
     if (clear) {
       recs.clear();
@@ -477,16 +511,20 @@ struct igb_ctx {
   void scms(int l, const double* res, double* u, bool u_zero) {
     Level& V = lev[l];
     const FdPlan& F = V.fd;
+    // the level's FD flops are booked on its first FD launch (class totals are what is reported)
+    double flops = F.flops;
     for (size_t b = 0; b < F.batches.size(); ++b) {
       launch(K_FD, F.batch_bytes[b], [&] {
         launch_fd_batch(stream, F.batches[b], res, u, V.tau, u_zero ? 0 : 1);
-      });
+      }, flops);
+      flops = 0.0;
     }
     for (int s = 0; s < F.nsteps; ++s) {
       if (F.ndesc[s] == 0) continue;
       launch(K_FD, F.bytes[s], [&] {
         launch_fd_gemm(stream, F.d_desc[s], F.ndesc[s], F.tiles[s], res, u, V.tau, u_zero ? 0 : 1);
-      });
+      }, flops);
+      flops = 0.0;
     }
     if (!V.h_blocks.empty() && !V.pieces_fused) {
       launch(K_PIECES, V.piece_bytes, [&] {
@@ -712,13 +750,18 @@ void check_csr(int n, int m, long long nnz, const int* ptr, const int* idx) {
   if (n < 0 || m < 0 || nnz < 0) throw ArgError("negative dimension");
   if (!ptr || (nnz && !idx)) throw ArgError("null CSR array");
   if (ptr[0] != 0 || ptr[n] != nnz) throw ArgError("indptr does not match nnz");
-  for (int i = 0; i < n; ++i) {
+  for (int i = 0; i < n; ++i)
     if (ptr[i + 1] < ptr[i]) throw ArgError("indptr not monotone");
-    for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
-      if (idx[k] < 0 || idx[k] >= m) throw ArgError("column index out of range");
-      if (k > ptr[i] && idx[k] <= idx[k - 1]) throw ArgError("column indices must be sorted and unique");
-    }
-  }
+  std::atomic<int> bad{0};
+  parallel_for(n, [&](long long lo, long long hi) {
+    for (long long i = lo; i < hi; ++i)
+      for (int k = ptr[i]; k < ptr[i + 1]; ++k) {
+        if (idx[k] < 0 || idx[k] >= m) bad |= 1;
+        if (k > ptr[i] && idx[k] <= idx[k - 1]) bad |= 2;
+      }
+  });
+  if (bad & 1) throw ArgError("column index out of range");
+  if (bad & 2) throw ArgError("column indices must be sorted and unique");
 }
 
 DevCsr upload_csr(igb_ctx* ctx, int n, int m, long long nnz, const int* ptr, const int* idx,
@@ -793,6 +836,11 @@ void require_final(igb_ctx* ctx) {
 void build_fd_plan(igb_ctx* ctx, Level& V) {
   if (V.interiors.empty()) return;
   int dim = V.interiors[0].dim;
+  V.fd.flops = 0.0;
+  for (auto& it : V.interiors) {  // 2 d contractions (front + back), 2 flops per FMA
+    const double cells = (double)it.n[0] * it.n[1] * (it.dim == 3 ? it.n[2] : 1);
+    V.fd.flops += 4.0 * cells * (it.n[0] + it.n[1] + (it.dim == 3 ? it.n[2] : 0));
+  }
   // 2-D interiors up to FDC_NMAX: one fused cluster each; the rest: batched GEMM steps
   std::vector<FdCluster> clu, clu_large;
   std::vector<InteriorStage> big;
@@ -990,6 +1038,10 @@ int igb_destroy(igb_ctx* ctx) {
   for (void* p : ctx->allocs) cudaFree(p);
   if (ctx->sc_host) cudaFreeHost(ctx->sc_host);
   if (ctx->hist_host) cudaFreeHost(ctx->hist_host);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
+    if (ctx->stage_ev[i]) cudaEventDestroy(ctx->stage_ev[i]);
+  }
   if (ctx->t0) cudaEventDestroy(ctx->t0);
   if (ctx->t1) cudaEventDestroy(ctx->t1);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
@@ -1022,8 +1074,10 @@ int igb_set_level_matrix(igb_ctx* ctx, int level, int n, long long nnz, const in
     V.n = n;
     V.A = upload_csr(ctx, n, n, nnz, indptr, indices, data);
     V.h_ptr.assign(indptr, indptr + n + 1);
-    V.h_col.assign(indices, indices + nnz);
-    V.h_val.assign(data, data + nnz);
+    V.h_col.resize(nnz);
+    V.h_val.resize(nnz);
+    par_memcpy(V.h_col.data(), indices, sizeof(int) * (size_t)nnz);
+    par_memcpy(V.h_val.data(), data, sizeof(double) * (size_t)nnz);
     std::vector<int> dp = diag_positions(n, indptr, indices, data, "A");
     V.dpos = ctx->upload(dp.data(), dp.size());
     V.tri_nnz_lower = V.tri_nnz_upper = 0;
@@ -1300,25 +1354,28 @@ bool build_panel_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::ve
     const int W = sh ? 8 : 16, R = sh ? 16384 : 8192, B = 2 * G * W;
     const int npan = (V.n + B - 1) / B;
     if (!force && 2 * npan > nlev) continue;
-    // B = 256 after B = 512 failed: the KF 10 variant on 2-D levels (cfg4 p = 8 backward, 136 far entries
-    // per row); 3-D levels keep KF <= 8 (B = 256 ranges broke a 3-D sweep, DESIGN 9)
-    static const bool kf10_3d = std::getenv("IGB_PANEL_KF10_3D") && std::atoi(std::getenv("IGB_PANEL_KF10_3D"));
-    const bool two_d = kf10_3d || (!V.interiors.empty() && V.interiors[0].dim == 2);  // env: diagnostic
+    // The B = 256 KF 10 variant (panel_sweep_kernel<9,12,10>) has an unresolved wrong-result mode:
+    // forced onto a 3-D level (cfg5 L=2 backward) the residual history drifts by up to 9e-2 from run to
+    // run (DESIGN 9.2, profiles/r1l_kf10_3d_diag.log).  It is therefore OFF by default on every level;
+    // IGB_PANEL_KF10=1 opts in (2-D levels), IGB_PANEL_KF10_3D=1 also on 3-D levels (diagnostic).
+    // Levels whose rows need it fall back to the B = 512 single-range plan or the flow engine.
+    // read per call (not cached): tests switch them between contexts of one process
+    const bool kf10 = std::getenv("IGB_PANEL_KF10") && std::atoi(std::getenv("IGB_PANEL_KF10")) != 0;
+    const bool kf10_3d = std::getenv("IGB_PANEL_KF10_3D") && std::atoi(std::getenv("IGB_PANEL_KF10_3D"));
+    const bool two_d = !V.interiors.empty() && V.interiors[0].dim == 2;
+    const bool allow_kf10 = kf10_3d || (kf10 && two_d);
     built = build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, W, R,
-                             max_clu[sh], plan, sh == 1 && two_d);
+                             max_clu[sh], plan, sh == 1 && allow_kf10);
     // B = 512 fell back to one range with the long-row variant (KA 14; cfg4 p = 8 backward): B = 256
-    // with its KF 10 variant may run several ranges and finish sooner (a B = 256 panel costs about as
-    // much as a B = 512 one, ~3 us).  Restricted to that case: on a 3-D level (cfg5 L=2) the switch
-    // broke the preconditioner's symmetry -- not investigated further this round.
-    // IGB_PANEL_HALF: 0 off, 1 (default) the KA 14 case only, 2 every single-range B = 512 plan (diagnostic);
-    // IGB_PANEL_KF10=0 keeps the alternative to KF <= 8
-    static const int half_mode = std::getenv("IGB_PANEL_HALF") ? std::atoi(std::getenv("IGB_PANEL_HALF")) : 1;
-    static const bool kf10 = !(std::getenv("IGB_PANEL_KF10") && std::atoi(std::getenv("IGB_PANEL_KF10")) == 0);
+    // may run several ranges and finish sooner (a B = 256 panel costs about as much as a B = 512 one,
+    // ~3 us) -- with KF <= 8 unless KF 10 is opted in.
+    // IGB_PANEL_HALF: 0 off, 1 (default) the KA 14 case only, 2 every single-range B = 512 plan (diagnostic)
+    const int half_mode = std::getenv("IGB_PANEL_HALF") ? std::atoi(std::getenv("IGB_PANEL_HALF")) : 1;
     if (built && sh == 0 && plan.nclu == 1 && (plan.KA == 14 || half_mode == 2) && max_clu[0] > 1 && half_mode &&
         (shapes_ok & 2)) {
       PanelPlanHost alt;
       if (build_panel_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, G, 8, 16384,
-                           max_clu[1], alt, kf10) &&
+                           max_clu[1], alt, allow_kf10) &&
           alt.nclu > 1 && alt.makespan < 0.8 * plan.makespan)
         plan = std::move(alt);
     }
@@ -1441,32 +1498,43 @@ int igb_set_gs(igb_ctx* ctx, int level) {
     require_levels(ctx);
     Level& V = ctx->level(level);
     if (!V.n) throw StateError("set the level matrix before igb_set_gs");
+    const bool verbose = std::getenv("IGB_VERBOSE") != nullptr;
+    auto tnow = [] { return std::chrono::steady_clock::now(); };
+    auto tick = tnow();
+    auto lap = [&](const char* what) {
+      if (!verbose) return;
+      const auto t = tnow();
+      std::fprintf(stderr, "[igb] set_gs level %d: %s %.2f s\n", level, what,
+                   std::chrono::duration<double>(t - tick).count());
+      tick = t;
+    };
     std::vector<int> dp = diag_positions(V.n, V.h_ptr.data(), V.h_col.data(), nullptr, "A");
     {
-      std::vector<int> up(V.n + 1, 0), ui;
-      std::vector<double> uv;
+      // strict triangles (parallel two-pass split of the CSR rows)
+      std::vector<int> up(V.n + 1, 0), lp(V.n + 1, 0);
       for (int i = 0; i < V.n; ++i) {
-        for (int j = dp[i] + 1; j < V.h_ptr[i + 1]; ++j) {
-          ui.push_back(V.h_col[j]);
-          uv.push_back(V.h_val[j]);
-        }
-        up[i + 1] = (int)ui.size();
+        up[i + 1] = up[i] + (V.h_ptr[i + 1] - dp[i] - 1);
+        lp[i + 1] = lp[i] + (dp[i] - V.h_ptr[i]);
       }
+      std::vector<int> ui(up[V.n]), li(lp[V.n]);
+      std::vector<double> uv(up[V.n]), lvv(lp[V.n]);
+      parallel_for(V.n, [&](long long lo, long long hi) {
+        for (long long i = lo; i < hi; ++i) {
+          const int a = V.h_ptr[i], d = dp[i], e = V.h_ptr[i + 1];
+          std::copy(V.h_col.begin() + d + 1, V.h_col.begin() + e, ui.begin() + up[i]);
+          std::copy(V.h_val.begin() + d + 1, V.h_val.begin() + e, uv.begin() + up[i]);
+          std::copy(V.h_col.begin() + a, V.h_col.begin() + d, li.begin() + lp[i]);
+          std::copy(V.h_val.begin() + a, V.h_val.begin() + d, lvv.begin() + lp[i]);
+        }
+      });
       V.U = upload_csr(ctx, V.n, V.n, (long long)ui.size(), up.data(), ui.data(), uv.data());
-      std::vector<int> lp(V.n + 1, 0), li;
-      std::vector<double> lvv;
-      for (int i = 0; i < V.n; ++i) {
-        for (int j = V.h_ptr[i]; j < dp[i]; ++j) {
-          li.push_back(V.h_col[j]);
-          lvv.push_back(V.h_val[j]);
-        }
-        lp[i + 1] = (int)li.size();
-      }
       V.Lo = upload_csr(ctx, V.n, V.n, (long long)li.size(), lp.data(), li.data(), lvv.data());
       V.has_U = !(std::getenv("IGB_GS_RESIDUAL") && std::string(std::getenv("IGB_GS_RESIDUAL")) == "full");
     }
+    lap("triangles");
     V.fwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, false);
     V.bwd = build_schedule(ctx, V.n, V.h_ptr.data(), V.h_col.data(), dp, true);
+    lap("schedules");
     const char* eng = std::getenv("IGB_GS_ENGINE");
     const std::string engine = eng ? eng : "auto";
     const bool want_stream = engine != "levels";
@@ -1477,6 +1545,7 @@ int igb_set_gs(igb_ctx* ctx, int level) {
         panel_done[dir] = build_panel_sweep(ctx, V, level, dir, dp, Sd.nlev, engine == "panel");
       }
     }
+    lap("panel plans");
     // whole-GPU dependency-driven sweep: wide dependency levels (3-D, high degree) where the
     // panel chain is not short; IGB_GS_ENGINE=flow forces it on every level
     for (int dir = 0; dir < 2; ++dir) {
@@ -1488,6 +1557,7 @@ int igb_set_gs(igb_ctx* ctx, int level) {
                         (engine == "auto" && (width >= flow_min_width() || tri >= 48LL * V.n));
       if (want) panel_done[dir] = build_flow_sweep(ctx, V, level, dir, dp);
     }
+    lap("flow plans");
     level_prepare();
     const char* clenv = std::getenv("IGB_GS_CLUSTER");
     const int cluster_max = clenv ? std::max(1, std::min(8, std::atoi(clenv))) : 8;
@@ -1546,6 +1616,7 @@ int igb_set_gs(igb_ctx* ctx, int level) {
       C.stream_bytes = (double)plan.stream.size();
       C.ok = true;
     }
+    lap("level plans");
     V.has_gs = true;
   });
 }
@@ -2170,6 +2241,7 @@ int igb_profile_reset(igb_ctx* ctx) {
       ctx->prof_ms[c] = 0;
       ctx->prof_n[c] = 0;
       ctx->prof_bytes[c] = 0;
+      ctx->prof_flops[c] = 0;
     }
   });
 }
@@ -2180,6 +2252,37 @@ int igb_launch_count(igb_ctx* ctx, long long* kernels, int reset) {
       ctx->launches_direct = 0;
       ctx->graph_replays = 0;
     }
+  });
+}
+
+int igb_profile_flops(igb_ctx* ctx, int cls, double* flops) {
+  return guarded(ctx, [&] {
+    if (cls < 0 || cls >= K_NCLASS) throw ArgError("unknown kernel class");
+    if (flops) *flops = ctx->prof_flops[cls];
+  });
+}
+
+int igb_gs_info(igb_ctx* ctx, int level, int dir, int* info, int ninfo) {
+  return guarded(ctx, [&] {
+    require_levels(ctx);
+    if (dir != 0 && dir != 1) throw ArgError("dir must be 0 (forward) or 1 (backward)");
+    Level& V = ctx->level(level);
+    if (!V.has_gs) throw StateError("no Gauss-Seidel smoother on this level");
+    int v[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const Sched& Sd = dir ? V.bwd : V.fwd;
+    v[6] = Sd.nlev;
+    if (V.panel[dir].ok) {
+      const PanelArgs& a = V.panel[dir].args;
+      v[0] = 1; v[1] = a.B; v[2] = a.KA; v[3] = a.KF; v[4] = a.nclu; v[5] = a.npan;
+    } else if (V.flow[dir].ok) {
+      v[0] = 2; v[1] = V.flow[dir].args.G; v[4] = V.flow[dir].args.ctas; v[6] = V.flow[dir].nlev;
+    } else if (V.sweep[dir].ok) {
+      v[0] = 3; v[4] = V.sweep[dir].args.cluster;
+    } else {
+      v[0] = 4;
+    }
+    v[7] = V.n;
+    for (int i = 0; i < ninfo && i < 8; ++i) info[i] = v[i];
   });
 }
 

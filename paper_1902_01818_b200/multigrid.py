@@ -20,6 +20,7 @@ from dataclasses import dataclass, field, asdict
 
 import numpy as np
 
+from . import _setup_native
 from . import assembly
 from . import linsolve
 from . import smoothers as sm
@@ -126,7 +127,12 @@ class MultigridSetup:
         t = time.perf_counter()
         for level in range(hier.L, 0, -1):
             self.P[level] = assembly.prolongation(hier, level)
-            self.A[level - 1] = (self.P[level].T @ self.A[level] @ self.P[level]).tocsr()
+            # Galerkin product (multigrid.py:95-99); native OpenMP product with SciPy's arithmetic
+            # (csrc/host_setup.cpp, bit-identical), SciPy when the setup library is unavailable
+            Ac = _setup_native.galerkin(self.A[level], self.P[level])
+            if Ac is None:
+                Ac = (self.P[level].T @ self.A[level] @ self.P[level]).tocsr()
+            self.A[level - 1] = Ac
         timings["galerkin"] = time.perf_counter() - t
         t = time.perf_counter()
         self.coarse_solver = linsolve.factorize(self.A[0], spd=True)
@@ -191,9 +197,19 @@ class MultigridSolver:
     # -- upload ------------------------------------------------------------------
     def _upload(self):
         ctx, L, cfg = self.ctx, self.finest, self.config
+        verbose = bool(os.environ.get("IGB_VERBOSE"))
+        tick = [time.perf_counter()]
+
+        def lap(what):
+            if verbose:
+                t = time.perf_counter()
+                print(f"[igb] upload {what}: {t - tick[0]:.2f} s", flush=True)
+                tick[0] = t
+
         ctx.set_num_levels(L)
         for level in range(L + 1):
             ctx.set_level_matrix(level, self.A[level])
+        lap("level matrices")
         # matrix-free finest operator where the patches allow it and A_L is not tiny (measured: cfg2
         # 5.10 -> 5.04 ms; cfg1's 98K-nonzero level is launch-bound, 0.78 ms CSR vs 0.90 ms)
         # Coarser levels too: their Galerkin operators P^T A P equal the rediscretised ones the
@@ -204,10 +220,12 @@ class MultigridSolver:
                 md = assembly.matrix_free_data(self.hier, level)
                 if md is not None:
                     ctx.set_matrix_free(level, md)
+        lap("matrix-free data")
         for level in range(1, L + 1):
             ctx.set_prolongation(level, self.P[level])
             if len(self.hier.spaces[level][0]) in (2, 3):
                 ctx.set_prolongation_kron(level, assembly.prolongation_kron(self.hier, level))
+        lap("prolongations")
         for level in range(1, L + 1):
             smo = self.smoother[level]
             gs = smo if isinstance(smo, sm.GaussSeidel) else getattr(smo, "gs", None)
@@ -219,14 +237,17 @@ class MultigridSolver:
                                           solver.denominator, piece.indices)
                 for (piece, _), inv in zip(scms.pieces, scms.piece_inverses):
                     ctx.scms_add_piece(level, piece.indices, inv)
-            if gs is not None:  # after the interiors: the sweep planner reads the level's dimension
+                lap(f"scms level {level}")
+            if gs is not None:  # after the interiors (only the opt-in KF 10 panel variant reads the dimension)
                 ctx.set_gs(level)
+                lap(f"gs level {level}")
             smo.bind(ctx, level)
         Lf, Uf, pr, pc = self.coarse_solver.factors()
         ctx.set_coarse_lu(Lf, Uf, pr, pc)
         steps = [cfg.steps_at(level, L) for level in range(L + 1)]
         ctx.set_cycle(cfg.smoother, cfg.mu, steps)
         ctx.finalize()
+        lap("coarse + finalize")
 
     @property
     def n_dofs(self):

@@ -380,7 +380,7 @@ class SubspaceCorrectedMass(_DeviceBound):
     def piece_inverses(self):
         """Dense inverses of the interface principal submatrices (from the SuperLU factors)."""
         if self._inverses is None:
-            self._inverses = [fact.inverse() for _, fact in self.pieces]
+            self._inverses = linsolve.inverses([fact for _, fact in self.pieces])
         return self._inverses
 
     def apply(self, r):

@@ -3,9 +3,11 @@
 Calls go through the C-ABI (libigb.so via ctypes).  Tolerances:
   * single operators (A@x, P@e, P^T r, GS sweeps, SCMS apply, coarse solve,
     one cycle): relative 2-norm difference <= 1e-12 (fp64, summation-order noise);
-  * PCG: identical iteration counts; residual history max_i |dh_i| / h_1 <= 1e-10
-    and per entry |dh_i| / h_i <= 1e-8 (1e-10 per entry is at
-    the fp64 floor for late entries); solution ||dx|| / ||x|| <= 1e-10;
+  * PCG: identical iteration counts; residual history per entry |dh_i| / h_i <= 1e-10
+    (the north star's bound) and max_i |dh_i| / h_1 <= 1e-10; solution ||dx|| / ||x|| <= 1e-10.
+    Exception: the SIPG L-shape (cfg3 family) is held to 3e-10 per entry -- SURVEY Appendix C
+    measured 3.5e-10 there for a CPU restatement that only re-orders sums (cond(A_0) = 1.2e6,
+    the over-penalised coarse SIPG operator); this build measures 2.1e-10 (profiles/r1l_configs.jsonl);
   * against the reference's own golden histories the same bounds apply.
 """
 
@@ -62,11 +64,22 @@ def test_operators_match_oracle(cfg, kw):
     assert rel(ctx.op("coarse", 0, x0, len(x0)), orc.coarse_solve(x0)) <= 1e-11
 
 
-def _check_history(h, ho, tag):
+HIST_TOL = 1e-10
+HIST_TOL_SIPG = 3e-10  # cfg3 family: the fp64 floor of SURVEY Appendix C (see module docstring)
+
+
+def hist_tol(cfg):
+    return HIST_TOL_SIPG if cfg == "cfg3" else HIST_TOL
+
+
+def _check_history(h, ho, tag, per_entry=HIST_TOL):
     h, ho = np.asarray(h), np.asarray(ho)
     assert len(h) == len(ho), tag
-    assert np.max(np.abs(h - ho)) / ho[0] <= 1e-10, tag
-    assert np.max(np.abs(h - ho) / ho) <= 1e-8, tag
+    d1 = np.max(np.abs(h - ho)) / ho[0]
+    de = np.max(np.abs(h - ho) / ho)
+    print(f"[hist] {tag}: max|dh|/h1 {d1:.2e}  per entry {de:.2e}")
+    assert d1 <= 1e-10, (tag, d1)
+    assert de <= per_entry, (tag, de)
 
 
 @pytest.mark.parametrize("golden,cfg,kw", SMALL_CASES + [("cfg2", "cfg2", {}), ("cfg3", "cfg3", {})])
@@ -75,11 +88,11 @@ def test_pcg_matches_oracle_and_reference(golden, cfg, kw):
     rep = solver.solve_pcg(f)
     xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert rep.iterations == itso and rep.converged
-    _check_history(rep.residuals, histo, "vs oracle")
+    _check_history(rep.residuals, histo, f"{golden} vs oracle", hist_tol(cfg))
     assert rel(rep.x, xo) <= 1e-10
     g = load_golden(golden)
     assert rep.iterations == int(g["its"])
-    _check_history(rep.residuals, g["hist"], "vs reference golden")
+    _check_history(rep.residuals, g["hist"], f"{golden} vs reference golden", hist_tol(cfg))
     assert rel(rep.x, g["x"]) <= 1e-10
 
 
@@ -272,7 +285,7 @@ def test_flow_engine_matches_oracle(cfg, kw, G):
     rep = solver.solve_pcg(f)
     xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert rep.iterations == itso
-    _check_history(rep.residuals, histo, "flow vs oracle")
+    _check_history(rep.residuals, histo, f"{cfg} flow vs oracle", hist_tol(cfg))
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
 
@@ -303,7 +316,7 @@ def test_kronecker_transfers_match_P(cfg, kw):
     rep = solver.solve_pcg(f)
     xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert rep.iterations == itso
-    _check_history(rep.residuals, histo, "kron transfers vs oracle")
+    _check_history(rep.residuals, histo, f"{cfg} kron transfers vs oracle", hist_tol(cfg))
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
 
@@ -328,7 +341,10 @@ def test_other_smoothers_and_cycles_match_oracle(smoother, nu, mu):
     rep = solver.solve_pcg(f)
     xo, itso, histo = orc.solve(f, tol=cfg.tol, max_iters=cfg.max_iters)
     assert rep.iterations == itso
-    _check_history(rep.residuals, histo, f"{smoother} nu={nu} mu={mu}")
+    # not a BASELINE configuration: plain GS on the SIPG L-shape needs up to 28 iterations, and the
+    # per-entry drift of the late (h ~ 1e-8) entries grows with the iteration count (measured 1.1e-9 for
+    # the W-cycle, 2.7e-10 for nu = 2); the h_1-relative bound stays 1e-10
+    _check_history(rep.residuals, histo, f"cfg3 {smoother} nu={nu} mu={mu}", 2e-9)
     assert rel(rep.x, xo) <= 1e-10
     solver.close()
 
@@ -416,3 +432,78 @@ def test_p6_backward_panel_far_slots_match_oracle():
             for _ in range(3):
                 assert np.array_equal(solver.ctx.op(op, level, x, n), first), (level, op)
             assert rel(first, ref(level, x)) <= 1e-12, (level, op)
+
+
+def _solver_with_env(cfg, kw, env):
+    import os
+    from paper_1902_01818_b200 import multigrid
+    pr, setup, f = get_setup(cfg, **kw)
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    return pr, setup, f, solver
+
+
+def test_kf10_panel_variant_is_opt_in():
+    """The B = 256 / KF 10 panel variant (known wrong-result mode, DESIGN 9.2) never runs by default,
+    IGB_PANEL_KF10=0 keeps it off, and IGB_PANEL_KF10=1 enables it on cfg4 p = 8's backward sweep."""
+    pr, setup, f, solver = _solver_with_env("cfg4", {"p": 8, "levels": 3}, {})
+    kfs = [solver.ctx.gs_info(l, d)["KF"] for l in range(1, 4) for d in (0, 1)]
+    solver.close()
+    assert 10 not in kfs
+    pr, setup, f, solver = _solver_with_env("cfg4", {"p": 8, "levels": 3}, {"IGB_PANEL_KF10": "0"})
+    assert 10 not in [solver.ctx.gs_info(l, d)["KF"] for l in range(1, 4) for d in (0, 1)]
+    solver.close()
+    # IGB_PANEL_HALF=2 lets every single-range B = 512 plan try the B = 256 alternative (at L = 3 the
+    # default KA 14 trigger does not fire)
+    pr, setup, f, solver = _solver_with_env("cfg4", {"p": 8, "levels": 3},
+                                            {"IGB_PANEL_KF10": "1", "IGB_PANEL_HALF": "2"})
+    info = solver.ctx.gs_info(3, 1)
+    print(f"[kf10] cfg4 p=8 L=3 level 3 backward with IGB_PANEL_KF10=1: {info}")
+    from oracle.solve import OracleSolver
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(71)
+    n = solver.A[3].shape[0]
+    x = rng.standard_normal(n)
+    first = solver.ctx.op("gs_bwd", 3, x, n)
+    for _ in range(19):
+        assert np.array_equal(solver.ctx.op("gs_bwd", 3, x, n), first)
+    assert rel(first, orc.gs_backward(3, x)) <= 1e-12
+    solver.close()
+
+
+def test_kf10_forced_on_3d_level():
+    """IGB_PANEL_KF10_3D=1 forces the KF 10 panel variant onto cfg5 L = 2 (the level where DESIGN 9.2
+    reproduced history drift): 20 repeated backward sweeps of every level bitwise identical and
+    within 1e-12 of SuperLU, and the PCG history within 1e-10 per entry of the oracle."""
+    pr, setup, f, solver = _solver_with_env("cfg5", {"levels": 2}, {"IGB_PANEL_KF10_3D": "1", "IGB_PANEL_HALF": "2"})
+    from oracle.solve import OracleSolver
+    orc = OracleSolver(setup.setup_bundle())
+    infos = {(l, d): solver.ctx.gs_info(l, d) for l in (1, 2) for d in (0, 1)}
+    print(f"[kf10-3d] {infos}")
+    assert any(i["engine"] == "panel" and i["KF"] == 10 for i in infos.values()), "KF 10 not exercised"
+    rng = np.random.default_rng(73)
+    # the cycle's post-smoothing runs the sweep in accumulate mode (u += T^-1 r on matrix-free levels):
+    # check one cycle first, then the plain sweeps
+    r = rng.standard_normal(solver.n_dofs)
+    print(f"[kf10-3d] cycle rel diff {rel(solver.cycle(2, r), orc.cycle(2, r)):.2e}")
+    for level in (1, 2):
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for op, ref in (("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward)):
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(19):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (level, op)
+    rep = solver.solve_pcg(f, check_spd=False)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, "cfg5 L=2 KF 10 forced")
+    solver.close()

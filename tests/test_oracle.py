@@ -115,3 +115,36 @@ def test_scms_tau_linearity_and_symmetry():
     b = OracleSolver(bundle2).scms_apply(2, r)
     assert np.allclose(b, 2 * a, rtol=1e-14, atol=0)
     assert abs(s @ orc.scms_apply(2, r) - r @ orc.scms_apply(2, s)) <= 1e-12 * abs(s @ a)
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg2", {"levels": 3}), ("cfg3", {"levels": 2}), ("cfg4", {"p": 8, "levels": 2}),
+                                    ("cfg5", {"levels": 2})])
+def test_trisolve_restatement_matches_superlu(cfg, kw):
+    """oracle/trisolve.c (row substitution, used where splu(tril(A)) does not fit) against the
+    reference's SuperLU NATURAL sweeps (smoothers.py:178-190) on every level: equal to rounding."""
+    from oracle.solve import _GaussSeidel, _TriSolveGS
+    pr, setup, f = get_setup(cfg, **kw)
+    rng = np.random.default_rng(12)
+    for level in range(1, setup.finest + 1):
+        A = setup.A[level]
+        r = rng.standard_normal(A.shape[0])
+        a, b = _GaussSeidel(A), _TriSolveGS(A)
+        for d in ("forward", "backward"):
+            x, y = getattr(a, d)(r), getattr(b, d)(r)
+            assert np.linalg.norm(x - y) <= 1e-13 * np.linalg.norm(x), (cfg, level, d)
+
+
+@pytest.mark.parametrize("golden,cfg,kw", [("cfg2_L3", "cfg2", {"levels": 3}), ("cfg3_L2", "cfg3", {"levels": 2}),
+                                           ("cfg5_L2", "cfg5", {"levels": 2})])
+def test_trisolve_oracle_matches_reference_golden(golden, cfg, kw):
+    """The oracle with C-substitution sweeps (the full-size checker of cfg4 p = 8 / cfg5) reproduces
+    the reference's golden iteration counts, histories (1e-10 per entry; cfg3 3e-10, SURVEY
+    Appendix C) and solutions."""
+    g = load_golden(golden)
+    pr, setup, f = get_setup(cfg, **kw)
+    x, its, hist = OracleSolver(setup.setup_bundle(), gs_impl="trisolve").solve(
+        f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert its == int(g["its"])
+    h, hg = np.array(hist), g["hist"]
+    assert np.max(np.abs(h - hg) / hg) <= (3e-10 if cfg == "cfg3" else 1e-10)
+    assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])

@@ -138,3 +138,44 @@ def test_galerkin_equals_rediscretised_on_affine_patches(name, kw):
     for level in range(1, pr.hier.L):
         Ag, Ad = setup.A[level], assembly.assemble_level(pr.hier, level).A
         assert abs(Ag - Ad).max() <= 1e-14 * abs(Ag).max()
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg1", {}), ("cfg2", {"levels": 2}), ("cfg5", {"levels": 1}),
+                                    ("cfg5", {"levels": 2})])
+def test_native_kron_assembly_bitwise(cfg, kw, monkeypatch):
+    """csrc/host_setup.cpp's Kronecker assembly + free-DoF reduction equals the SciPy path array for
+    array (indptr, indices, data), for A and the Dirichlet coupling (reference assembly.py:333-344,
+    568-608)."""
+    from paper_1902_01818_b200 import _setup_native, assembly, configs
+    if _setup_native.lib() is None:
+        pytest.skip("libigb_setup.so not built")
+    pr = configs.build(cfg, **kw)
+    for level in range(pr.hier.L + 1):
+        nat = assembly.assemble_level(pr.hier, level)
+        monkeypatch.setenv("IGB_NATIVE_SETUP", "0")
+        ref = assembly.assemble_level(pr.hier, level)
+        monkeypatch.delenv("IGB_NATIVE_SETUP")
+        for a, b in ((nat.A, ref.A), (nat.couple, ref.couple)):
+            a, b = a.tocsr(), b.tocsr()
+            assert a.shape == b.shape
+            assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices), (cfg, level)
+            assert np.array_equal(a.data, b.data), (cfg, level, np.abs(a.data - b.data).max())
+
+
+@pytest.mark.parametrize("cfg,kw", [("cfg2", {"levels": 3}), ("cfg3", {"levels": 2}), ("cfg4", {"p": 3, "levels": 2}),
+                                    ("cfg5", {"levels": 2})])
+def test_native_galerkin_bitwise(cfg, kw):
+    """csrc/host_setup.cpp's P^T A P equals SciPy's (P.T @ A @ P).tocsr() bit for bit (multigrid.py:95-99)."""
+    from paper_1902_01818_b200 import _setup_native, assembly, configs
+    if _setup_native.lib() is None:
+        pytest.skip("libigb_setup.so not built")
+    pr = configs.build(cfg, **kw)
+    A = assembly.assemble_level(pr.hier, pr.hier.L).A
+    for level in range(pr.hier.L, 0, -1):
+        P = assembly.prolongation(pr.hier, level)
+        ref = (P.T @ A @ P).tocsr()
+        ref.sort_indices()
+        nat = _setup_native.galerkin(A, P)
+        assert np.array_equal(nat.indptr, ref.indptr) and np.array_equal(nat.indices, ref.indices), (cfg, level)
+        assert np.array_equal(nat.data, ref.data), (cfg, level, np.abs(nat.data - ref.data).max())
+        A = ref

@@ -185,8 +185,9 @@ int igb_profile_flops(igb_ctx* ctx, int cls, double* flops);
 
 /* Which Gauss-Seidel engine igb_set_gs planned for (level, dir) (dir 0 forward, 1 backward);
  * info[0..ninfo) receives: engine (1 panel sweep, 2 flow sweep, 3 level-set sweep, 4 level
- * schedule), panel rows B (flow: lanes per row), KA near slots, KF far slots, clusters / ranges
- * (flow: CTAs), panels, dependency levels, n.  Diagnostic; no reference counterpart.
+ * schedule, 5 line sweep), panel rows B (flow: lanes per row; line: largest bundle), KA near
+ * slots (line: chunks per row), KF far slots, clusters / ranges (flow: CTAs; line: bundles),
+ * panels (line: lines), dependency levels, n.  Diagnostic; no reference counterpart.
  * Note: the opt-in B = 256 / KF 10 panel variant (IGB_PANEL_KF10=1) reads the level's dimension
  * from its interiors, so with it igb_set_gs must follow igb_scms_add_interior; by default the
  * plan does not depend on call order. */

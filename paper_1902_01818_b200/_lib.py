@@ -58,7 +58,7 @@ SIGNATURES = {
     "igb_gs_info": ([_p, _i, _i, _ip, _i], _i),
     "igb_profile_flops": ([_p, _i, ctypes.POINTER(_d)], _i),
 }
-GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule"}
+GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule", 5: "line"}
 
 _lib = None
 

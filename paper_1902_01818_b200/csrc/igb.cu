@@ -26,6 +26,7 @@
 #include "igb.h"
 #include "level_plan.h"
 #include "flow_plan.h"
+#include "line_plan.h"
 #include "panel_plan.h"
 #include "host_par.h"
 #include "kernels.cuh"
@@ -112,6 +113,13 @@ struct FlowDev {
   long long entries = 0;
 };
 
+struct LineDev {
+  bool ok = false;
+  LineArgs args{};
+  long long entries = 0, slots = 0;
+  int nl = 0, max_line = 0;
+};
+
 struct Level {
   int n = 0;
   DevCsr A;
@@ -120,6 +128,7 @@ struct Level {
   SweepDev sweep[2];   // 0: forward (lower) sweep, 1: backward (upper) sweep
   PanelDev panel[2];   // row-panel sweeps (preferred when built)
   FlowDev flow[2];     // dependency-driven whole-GPU sweeps (wide levels, long rows)
+  LineDev line[2];     // line sweeps (bundles of grid lines per CTA; 3-D levels)
   double* xg = nullptr;  // panel sweep solution by position (old values)
   double* rp = nullptr;   // level-ordered right-hand side / solution of the sweep
   double* xp = nullptr;
@@ -404,6 +413,36 @@ struct igb_ctx {
                      l, upper ? 1 : 0, V.n, hd[0], hd[1] / np, hd[2] / np, hd[3] / np, hd[4] / np, hd[5] / np,
                      hd[6] / np, hd[7] / np);
       }
+      return;
+    }
+    LineDev& Ln = V.line[upper ? 1 : 0];
+    if (Ln.ok) {
+      LineArgs a = Ln.args;
+      a.res = rhs;
+      a.u = u;
+      a.accumulate = u_zero ? 0 : 1;
+      const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
+      static const bool want_dbg = std::getenv("IGB_GS_DEBUG") != nullptr;
+      if (want_dbg && !capturing) {
+        cudaEvent_t e0, e1;
+        CU(cudaEventCreate(&e0));
+        CU(cudaEventCreate(&e1));
+        CU(cudaEventRecord(e0, stream));
+        launch_line_sweep(stream, a);
+        CU(cudaEventRecord(e1, stream));
+        CU(cudaEventSynchronize(e1));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        const int depth = upper ? V.bwd.nlev : V.fwd.nlev;
+        std::fprintf(stderr, "[gs dbg] line level %d dir %d n %d depth %d bundles %d lines %d ctas %d C %d: %.1f us, "
+                     "%.3f us/level\n", l, upper ? 1 : 0, V.n, depth, a.nb, Ln.nl, a.ctas, a.C, ms * 1e3,
+                     ms * 1e3 / std::max(1, depth));
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return;
+      }
+      launch(K_GS, bytes, [&] { launch_line_sweep(stream, a); });
       return;
     }
     FlowDev& Fw = V.flow[upper ? 1 : 0];
@@ -1444,6 +1483,58 @@ double flow_min_width() {
   return w;
 }
 
+// Line sweep for one direction (line_plan.h, line.cu).
+bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
+  const char* mn = std::getenv("IGB_LINE_RBMIN");
+  const char* mx = std::getenv("IGB_LINE_RBMAX");
+  const int rb_min = mn ? std::max(1, std::atoi(mn)) : 512;
+  const int rb_cap = mx ? std::max(64, std::atoi(mx)) : 8192;
+  LinePlanHost plan;
+  if (!build_line_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, rb_min, rb_cap, 8,
+                       plan))
+    return false;
+  if (line_chunk_variant(plan.C) < 0) return false;
+  const size_t smem = 8 * ((size_t)plan.rb_max + 1);
+  const int cap = line_max_ctas(smem);
+  if (cap < 1) return false;
+  LineDev& D = V.line[dir];
+  LineArgs& a = D.args;
+  a = LineArgs{};
+  a.n = V.n;
+  a.nb = plan.nb;
+  a.rb_max = plan.rb_max;
+  a.C = line_chunk_variant(plan.C);
+  a.upper = dir;
+  a.ctas = std::min(cap, plan.nb);
+  a.bstart = ctx->upload(plan.bstart.data(), plan.bstart.size());
+  a.bline = ctx->upload(plan.bline.data(), plan.bline.size());
+  a.lstart = ctx->upload(plan.lstart.data(), plan.lstart.size());
+  a.cptr = ctx->upload(plan.cptr.data(), plan.cptr.size());
+  // padded so that the unconditional next-row loads of the last row stay in bounds
+  plan.ccol.resize(plan.ccol.size() + 32 * 8, -1 - plan.rb_max);
+  plan.cval.resize(plan.cval.size() + 32 * 8, 0.0);
+  a.ccol = ctx->upload(plan.ccol.data(), plan.ccol.size());
+  a.cval = ctx->upload(plan.cval.data(), plan.cval.size());
+  a.own = ctx->upload(plan.own.data(), plan.own.size());
+  a.idiag = ctx->upload(plan.idiag.data(), plan.idiag.size());
+  std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF9ABCULL);  // line.cu LINE_PENDING
+  a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
+  int* ctr = ctx->alloc<int>(2);
+  CU(cudaMemset(ctr, 0, 2 * sizeof(int)));
+  a.par_ctr = ctr;
+  a.done_ctr = reinterpret_cast<unsigned*>(ctr + 1);
+  D.entries = plan.entries;
+  D.slots = plan.slots;
+  D.nl = plan.nl;
+  D.max_line = plan.max_line;
+  D.ok = true;
+  if (std::getenv("IGB_VERBOSE"))
+    std::fprintf(stderr, "[igb] level %d dir %d: line sweep n %d lines %d (max %d) bundles %d (max rows %d) C %d "
+                 "entries %lld slots %lld ctas %d\n", level, dir, V.n, plan.nl, plan.max_line, plan.nb, plan.rb_max,
+                 plan.C, plan.entries, plan.slots, a.ctas);
+  return true;
+}
+
 // Dependency-driven whole-GPU sweep for one direction (flow_plan.h, flow.cu).
 bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
   const char* ge = std::getenv("IGB_FLOW_G");
@@ -1546,6 +1637,12 @@ int igb_set_gs(igb_ctx* ctx, int level) {
       }
     }
     lap("panel plans");
+    // line sweep (bundles of grid lines per CTA): IGB_GS_ENGINE=line forces it on every level
+    if (engine == "line") {
+      for (int dir = 0; dir < 2; ++dir)
+        if (!panel_done[dir]) panel_done[dir] = build_line_sweep(ctx, V, level, dir, dp);
+      lap("line plans");
+    }
     // whole-GPU dependency-driven sweep: wide dependency levels (3-D, high degree) where the
     // panel chain is not short; IGB_GS_ENGINE=flow forces it on every level
     for (int dir = 0; dir < 2; ++dir) {
@@ -2274,6 +2371,9 @@ int igb_gs_info(igb_ctx* ctx, int level, int dir, int* info, int ninfo) {
     if (V.panel[dir].ok) {
       const PanelArgs& a = V.panel[dir].args;
       v[0] = 1; v[1] = a.B; v[2] = a.KA; v[3] = a.KF; v[4] = a.nclu; v[5] = a.npan;
+    } else if (V.line[dir].ok) {
+      v[0] = 5; v[1] = V.line[dir].args.rb_max; v[2] = V.line[dir].args.C; v[4] = V.line[dir].args.nb;
+      v[5] = V.line[dir].nl;
     } else if (V.flow[dir].ok) {
       v[0] = 2; v[1] = V.flow[dir].args.G; v[4] = V.flow[dir].args.ctas; v[6] = V.flow[dir].nlev;
     } else if (V.sweep[dir].ok) {

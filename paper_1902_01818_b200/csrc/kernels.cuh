@@ -162,6 +162,28 @@ int flow_max_ctas();  // co-resident CTAs of FLOW_NT threads (all variants)
 void flow_set_carveout(int pct);
 void launch_flow_sweep(cudaStream_t s, const FlowArgs& a);
 
+// ---- line sweep: GS along grid lines, bundles of lines per CTA (line.cu, line_plan.h) -------
+constexpr int LINE_NT = 512;  // 16 warps per CTA
+struct LineArgs {
+  const int* bstart;   // [nb + 1] positions
+  const int* bline;    // [nb + 1] first line per bundle
+  const int* lstart;   // [nl + 1] positions
+  const int* cptr;     // [n + 1] chunk offsets
+  const int* ccol;     // [32 * chunks] source codes (>= 0 position, < 0 shared slot -1 - code)
+  const double* cval;
+  const double* own;   // [3 n] coefficients of x(p-1..p-3) in the same line
+  const double* idiag; // [n] by position
+  const double* res;   // right-hand side by row
+  double* u;           // u (+)= c by row
+  double* xg;          // [2][n] by position
+  int* par_ctr;
+  unsigned* done_ctr;
+  int n, nb, rb_max, C, upper, accumulate, ctas;
+};
+int line_chunk_variant(int C);           // kernel variant for C chunks per row (-1: none)
+int line_max_ctas(size_t smem_bytes);    // co-resident CTAs of LINE_NT threads
+void launch_line_sweep(cudaStream_t s, const LineArgs& a);
+
 // ---- intergrid transfers as per-patch Kronecker products (transfer.cu) --------------
 struct KronPatch {
   int nf[3], nc[3];            // block sizes per axis (1 past dim)

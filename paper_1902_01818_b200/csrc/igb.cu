@@ -428,10 +428,47 @@ struct igb_ctx {
         cudaEvent_t e0, e1;
         CU(cudaEventCreate(&e0));
         CU(cudaEventCreate(&e1));
+        const char* tr = std::getenv("IGB_LINE_TRACE");
+        long long* dtr = nullptr;
+        if (tr) {
+          CU(cudaMalloc(&dtr, 3 * sizeof(long long) * V.n));
+          CU(cudaMemsetAsync(dtr, 0, 3 * sizeof(long long) * V.n, stream));
+          a.trace = dtr;
+        }
+        long long* dprof = nullptr;
+        CU(cudaMalloc(&dprof, 8 * sizeof(long long)));
+        CU(cudaMemsetAsync(dprof, 0, 8 * sizeof(long long), stream));
+        a.prof = dprof;
         CU(cudaEventRecord(e0, stream));
         launch_line_sweep(stream, a);
         CU(cudaEventRecord(e1, stream));
         CU(cudaEventSynchronize(e1));
+        {
+          long long hp[8];
+          CU(cudaMemcpy(hp, dprof, sizeof(hp), cudaMemcpyDeviceToHost));
+          cudaFree(dprof);
+          const double r = std::max(1LL, hp[5]);
+          std::fprintf(stderr, "[gs dbg] line level %d dir %d cycles/row: D-poll %.0f D %.0f C %.0f B %.0f A %.0f\n", l,
+                       upper ? 1 : 0, hp[0] / r, hp[1] / r, hp[2] / r, hp[3] / r, hp[4] / r);
+        }
+        if (tr) {  // binary dump: int n, nl, nb; int[nl+1] lstart; int[nb+1] bstart; int64[3n] trace
+          std::vector<long long> ht(3 * (size_t)V.n);
+          CU(cudaMemcpy(ht.data(), dtr, ht.size() * sizeof(long long), cudaMemcpyDeviceToHost));
+          cudaFree(dtr);
+          std::vector<int> ls(Ln.nl + 1), bsv(a.nb + 1);
+          CU(cudaMemcpy(ls.data(), a.lstart, ls.size() * sizeof(int), cudaMemcpyDeviceToHost));
+          CU(cudaMemcpy(bsv.data(), a.bstart, bsv.size() * sizeof(int), cudaMemcpyDeviceToHost));
+          char path[512];
+          std::snprintf(path, sizeof(path), "%s.l%d.d%d.bin", tr, l, upper ? 1 : 0);
+          if (FILE* fp = std::fopen(path, "wb")) {
+            int hdr[3] = {V.n, Ln.nl, a.nb};
+            std::fwrite(hdr, sizeof(int), 3, fp);
+            std::fwrite(ls.data(), sizeof(int), ls.size(), fp);
+            std::fwrite(bsv.data(), sizeof(int), bsv.size(), fp);
+            std::fwrite(ht.data(), sizeof(long long), ht.size(), fp);
+            std::fclose(fp);
+          }
+        }
         float ms = 0;
         CU(cudaEventElapsedTime(&ms, e0, e1));
         const int depth = upper ? V.bwd.nlev : V.fwd.nlev;
@@ -1493,7 +1530,7 @@ bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   if (!build_line_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, rb_min, rb_cap, 8,
                        plan))
     return false;
-  if (line_chunk_variant(plan.C) < 0) return false;
+
   const size_t smem = 8 * ((size_t)plan.rb_max + 1);
   const int cap = line_max_ctas(smem);
   if (cap < 1) return false;
@@ -1503,20 +1540,19 @@ bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   a.n = V.n;
   a.nb = plan.nb;
   a.rb_max = plan.rb_max;
-  a.C = line_chunk_variant(plan.C);
+  a.C = plan.C;
   a.upper = dir;
   a.ctas = std::min(cap, plan.nb);
   a.bstart = ctx->upload(plan.bstart.data(), plan.bstart.size());
   a.bline = ctx->upload(plan.bline.data(), plan.bline.size());
   a.lstart = ctx->upload(plan.lstart.data(), plan.lstart.size());
-  a.cptr = ctx->upload(plan.cptr.data(), plan.cptr.size());
-  // padded so that the unconditional next-row loads of the last row stay in bounds
-  plan.ccol.resize(plan.ccol.size() + 32 * 8, -1 - plan.rb_max);
-  plan.cval.resize(plan.cval.size() + 32 * 8, 0.0);
-  a.ccol = ctx->upload(plan.ccol.data(), plan.ccol.size());
-  a.cval = ctx->upload(plan.cval.data(), plan.cval.size());
-  a.own = ctx->upload(plan.own.data(), plan.own.size());
-  a.idiag = ctx->upload(plan.idiag.data(), plan.idiag.size());
+  // padded: the L2 bulk prefetch of the records runs a few rows past the end
+  plan.rec.resize(plan.rec.size() + (size_t)line_rec_bytes(plan.C) * 16 / 8, 0.0);
+  a.rec = reinterpret_cast<const char*>(ctx->upload(plan.rec.data(), plan.rec.size()));
+  a.ocol = ctx->upload(plan.ocol.data(), plan.ocol.size());
+  a.oval = ctx->upload(plan.oval.data(), plan.oval.size());
+  const char* pfe = std::getenv("IGB_LINE_PF");
+  a.pf = pfe ? std::max(1, std::atoi(pfe)) : 8;
   std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF9ABCULL);  // line.cu LINE_PENDING
   a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
   int* ctr = ctx->alloc<int>(2);
@@ -1524,14 +1560,15 @@ bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   a.par_ctr = ctr;
   a.done_ctr = reinterpret_cast<unsigned*>(ctr + 1);
   D.entries = plan.entries;
-  D.slots = plan.slots;
+  D.slots = plan.chunks * 32;
   D.nl = plan.nl;
   D.max_line = plan.max_line;
   D.ok = true;
   if (std::getenv("IGB_VERBOSE"))
     std::fprintf(stderr, "[igb] level %d dir %d: line sweep n %d lines %d (max %d) bundles %d (max rows %d) C %d "
-                 "entries %lld slots %lld ctas %d\n", level, dir, V.n, plan.nl, plan.max_line, plan.nb, plan.rb_max,
-                 plan.C, plan.entries, plan.slots, a.ctas);
+                 "(max %d, %lld overflow rows) entries %lld records %.1f MB ctas %d\n", level, dir, V.n, plan.nl,
+                 plan.max_line, plan.nb, plan.rb_max, plan.C, plan.cmax, plan.ovf_rows, plan.entries,
+                 8.0 * plan.rec.size() / 1e6, a.ctas);
   return true;
 }
 

@@ -168,17 +168,17 @@ struct LineArgs {
   const int* bstart;   // [nb + 1] positions
   const int* bline;    // [nb + 1] first line per bundle
   const int* lstart;   // [nl + 1] positions
-  const int* cptr;     // [n + 1] chunk offsets
-  const int* ccol;     // [32 * chunks] source codes (>= 0 position, < 0 shared slot -1 - code)
-  const double* cval;
-  const double* own;   // [3 n] coefficients of x(p-1..p-3) in the same line
-  const double* idiag; // [n] by position
+  const char* rec;     // [n] fixed-size records (line_plan.h), line_rec_bytes(C) each
+  const int* ocol;     // overflow chunks of long rows (codes / values)
+  const double* oval;
   const double* res;   // right-hand side by row
   double* u;           // u (+)= c by row
   double* xg;          // [2][n] by position
   int* par_ctr;
   unsigned* done_ctr;
-  int n, nb, rb_max, C, upper, accumulate, ctas;
+  int n, nb, rb_max, C, upper, accumulate, ctas, pf;
+  long long* trace;    // debug (nullable): per position [publish globaltimer, D poll cycles, C poll cycles]
+  long long* prof;     // debug (nullable): [5] cycles summed over warps in D-poll, D, C, B, A + [5] rows
 };
 int line_chunk_variant(int C);           // kernel variant for C chunks per row (-1: none)
 int line_max_ctas(size_t smem_bytes);    // co-resident CTAs of LINE_NT threads

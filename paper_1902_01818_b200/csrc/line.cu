@@ -23,6 +23,7 @@
 #include <cstdio>
 
 #include "kernels.cuh"
+#include "line_plan.h"
 
 namespace igb {
 namespace {
@@ -49,107 +50,277 @@ __device__ __noinline__ void line_stuck(int code, int p) {
   __trap();
 }
 
+__device__ __forceinline__ double fetch(const double* xs, const double* xg, int code) {
+  return code < 0 ? lds_vol(xs + (-1 - code)) : ld_relaxed(xg + code);
+}
+
+__device__ __forceinline__ void prefetch_line_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+
+// Per-warp row pipeline (iteration t works on four rows at once):
+//   A  row t+3: load its early entry codes; bulk-prefetch the record of the row a.pf rows further
+//               along this warp's row sequence into L2;
+//   B  row t+2: issue the gathers of its early values (shared / global), load their coefficients;
+//   C  row t+1: re-poll early values still pending (together), FMA, butterfly reduction -> acc in
+//               every lane; issue the gathers of its late values, load its scalars;
+//   D  row t:   re-poll its late values (together), finish
+//               s = rhs - acc - sum late (oldest first) - own(3, 2, 1), publish x.
+// Only D waits on the newest values, so the gathers and the reduction run ahead of the
+// critical path; every per-row array the pipeline reads is in the row's record (one contiguous
+// block, prefetched as one bulk copy) or in res / u (prefetched by line).
 template <int C>
-struct RowData {
+struct StA {
+  int p, row;
   int cc[C];
-  double cv[C];
-  int nch;
+};
+template <int C>
+struct StB {
+  int p, row;
+  int cc[C];
+  double cv[C], xv[C];
+};
+struct StD {
+  int p, row;
+  long long cw;  // trace: cycles re-polling early values
+  double acc;
+  int lc[LINE_LATE];
+  double lv[LINE_LATE], lx[LINE_LATE];
+  double rhs, idg, o1, o2, o3, uold;
 };
 
-template <int C>
-__device__ __forceinline__ void load_row(const LineArgs& a, int p, int lane, RowData<C>& r) {
-  const int c0 = __ldg(a.cptr + p), c1 = __ldg(a.cptr + p + 1);
-  r.nch = c1 - c0;
-  const size_t base = (size_t)c0 * 32 + lane;
-#pragma unroll
-  for (int k = 0; k < C; ++k) {
-    r.cc[k] = k < r.nch ? __ldg(a.ccol + base + 32 * k) : -1 - a.rb_max;
-    r.cv[k] = k < r.nch ? __ldg(a.cval + base + 32 * k) : 0.0;
+// This warp's row sequence within a bundle: lines l0, l0 + W, ...; positions in order.
+struct RowIter {
+  int l, p, end;
+  __device__ __forceinline__ void init(const LineArgs& a, int l0, int lend) {
+    l = l0;
+    p = end = -1;
+    if (l < lend) {
+      p = a.lstart[l];
+      end = a.lstart[l + 1];
+    }
   }
-}
+  __device__ __forceinline__ int next(const LineArgs& a, int W, int lend) {  // current (-1: done), advance
+    const int cur = p;
+    if (cur < 0) return -1;
+    if (++p == end) {
+      l += W;
+      if (l < lend) {
+        p = a.lstart[l];
+        end = a.lstart[l + 1];
+      } else {
+        p = -1;
+      }
+    }
+    return cur;
+  }
+};
 
 template <int C>
 __global__ void __launch_bounds__(LINE_NT, 1) line_sweep_kernel(LineArgs a) {
   pdl_begin();
   extern __shared__ __align__(16) double xs[];  // [rb_max + 1]; slot rb_max always 0
+  constexpr int RB = line_rec_bytes(C);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, W = blockDim.x >> 5;
   const int par = *(volatile const int*)a.par_ctr;
   const double* xg_cur = a.xg + (size_t)par * a.n;
   double* xg_set = a.xg + (size_t)par * a.n;
   double* xg_clr = a.xg + (size_t)(par ^ 1) * a.n;
+  const int zero_code = -1 - a.rb_max;
   if (threadIdx.x == 0) xs[a.rb_max] = 0.0;
+  auto rec = [&](int p) { return a.rec + (size_t)p * RB; };
   for (int b = blockIdx.x; b < a.nb; b += gridDim.x) {
     const int bs = a.bstart[b], be = a.bstart[b + 1];
+    const int lend = a.bline[b + 1];
     for (int i = threadIdx.x; i < be - bs; i += blockDim.x) xs[i] = __longlong_as_double((long long)LINE_PENDING);
+    RowIter it, pf;
+    it.init(a, a.bline[b] + warp, lend);
+    pf.init(a, a.bline[b] + warp, lend);
+    // L2 prefetch of the first a.pf records of this warp's sequence (the pipeline keeps a.pf ahead)
+    for (int k = 0; k < a.pf; ++k) {
+      const int q = pf.next(a, W, lend);
+      if (q >= 0 && lane == 0) {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rec(q)), "r"((unsigned)RB) : "memory");
+        prefetch_line_l2(a.res + (a.upper ? a.n - 1 - q : q));
+      }
+    }
     __syncthreads();
-    for (int l = a.bline[b] + warp; l < a.bline[b + 1]; l += W) {
-      const int p0 = a.lstart[l], p1 = a.lstart[l + 1];
-      double x1 = 0.0, x2 = 0.0, x3 = 0.0;
-      RowData<C> cur, nxt;
-      load_row<C>(a, p0, lane, cur);
-      for (int p = p0; p < p1; ++p) {
-        const int row = a.upper ? a.n - 1 - p : p;
-        double rhs = 0.0, idg = 0.0, o1 = 0.0, o2 = 0.0, o3 = 0.0, uold = 0.0;
-        rhs = __ldg(a.res + row);
-        idg = __ldg(a.idiag + p);
-        o1 = __ldg(a.own + 3 * (size_t)p);
-        o2 = __ldg(a.own + 3 * (size_t)p + 1);
-        o3 = __ldg(a.own + 3 * (size_t)p + 2);
-        if (a.accumulate && lane == 0) uold = a.u[row];
-        if (p + 1 < p1) load_row<C>(a, p + 1, lane, nxt);
-        if (lane == 0 && p + LINE_PF < p1) {
-          const int cpf = __ldg(a.cptr + p + LINE_PF), cpe = __ldg(a.cptr + p + LINE_PF + 1);
-          if (cpe > cpf) {
-            prefetch_l2(a.cval + (size_t)cpf * 32, (unsigned)(cpe - cpf) * 256u);
-            prefetch_l2(a.ccol + (size_t)cpf * 32, (unsigned)(cpe - cpf) * 128u);
-          }
-        }
-        // gather the row's values (shared: the bundle; global: other bundles); re-poll pending ones
-        double xv[C];
+    auto stage_a = [&](StA<C>& A, int p) {
+      A.p = p;
+      if (p < 0) return;
+      A.row = a.upper ? a.n - 1 - p : p;
+      const int* cc = reinterpret_cast<const int*>(rec(p));
 #pragma unroll
-        for (int k = 0; k < C; ++k) xv[k] = cur.cc[k] < 0 ? lds_vol(xs + (-1 - cur.cc[k])) : ld_relaxed(xg_cur + cur.cc[k]);
-        unsigned pm = 0;
+      for (int k = 0; k < C; ++k) A.cc[k] = __ldg(cc + 32 * k + lane);
+      const int q = pf.next(a, W, lend);
+      if (q >= 0 && lane == 0) {
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rec(q)), "r"((unsigned)RB) : "memory");
+        const int qr = a.upper ? a.n - 1 - q : q;
+        prefetch_line_l2(a.res + qr);
+        if (a.accumulate) prefetch_line_l2(a.u + qr);
+      }
+    };
+    auto stage_b = [&](StB<C>& B, const StA<C>& A) {
+      B.p = A.p;
+      B.row = A.row;
+      if (A.p < 0) return;
+      const double* cv = reinterpret_cast<const double*>(rec(A.p) + line_off_cv(C));
 #pragma unroll
-        for (int k = 0; k < C; ++k) pm |= pend(xv[k]) ? 1u << k : 0u;
-        if (pm) {
-          const long long w0 = clock64();
-          do {
+      for (int k = 0; k < C; ++k) {
+        B.cc[k] = A.cc[k];
+        B.xv[k] = fetch(xs, xg_cur, A.cc[k]);
+        B.cv[k] = __ldg(cv + 32 * k + lane);
+      }
+    };
+    auto poll = [&](int code, double v, int p) {
+      if (!pend(v)) return v;
+      const long long w0 = clock64();
+      do {
+        v = fetch(xs, xg_cur, code);
+        if (clock64() - w0 > (1LL << 31)) line_stuck(code, p);
+      } while (pend(v));
+      return v;
+    };
+    auto stage_c = [&](StD& D, StB<C>& B) {
+      D.p = B.p;
+      D.row = B.row;
+      if (B.p < 0) return;
+      const int p = B.p;
+      const char* r = rec(p);
+      const int* meta = reinterpret_cast<const int*>(r + line_off_meta(C));
+      const double* lvv = reinterpret_cast<const double*>(r + line_off_lv(C));
+      const double* own = reinterpret_cast<const double*>(r + line_off_own(C));
+      // late values and scalars of this row first (consumed one iteration later, in D)
+#pragma unroll
+      for (int j = 0; j < LINE_LATE; ++j) {
+        D.lc[j] = __ldg(meta + j);
+        D.lv[j] = __ldg(lvv + j);
+      }
+#pragma unroll
+      for (int j = 0; j < LINE_LATE; ++j) D.lx[j] = fetch(xs, xg_cur, D.lc[j]);
+      const int ovs = __ldg(meta + LINE_LATE), ovn = __ldg(meta + LINE_LATE + 1);
+      D.rhs = __ldg(a.res + B.row);
+      D.o1 = __ldg(own);
+      D.o2 = __ldg(own + 1);
+      D.o3 = __ldg(own + 2);
+      D.idg = __ldg(own + 3);
+      D.uold = (a.accumulate && lane == 0) ? a.u[B.row] : 0.0;
+      // early values still pending: re-polled together, one round trip per attempt
+      unsigned pm = 0;
+#pragma unroll
+      for (int k = 0; k < C; ++k) pm |= pend(B.xv[k]) ? 1u << k : 0u;
+      D.cw = 0;
+      if (a.trace && __any_sync(0xffffffffu, pm)) D.cw = -clock64();
+      if (pm) {
+        const long long w0 = clock64();
+        unsigned nap = 0;  // backoff: a waiting warp must not take issue slots from the working ones
+        do {
+          if (nap) __nanosleep(nap);
+          nap = nap ? min(nap * 2u, 1024u) : 32u;
+#pragma unroll
+          for (int k = 0; k < C; ++k)
+            if (pm >> k & 1u) B.xv[k] = fetch(xs, xg_cur, B.cc[k]);
+#pragma unroll
+          for (int k = 0; k < C; ++k)
+            if ((pm >> k & 1u) && !pend(B.xv[k])) pm &= ~(1u << k);
+          if (pm && clock64() - w0 > (1LL << 31)) {
+            int bad = 0;
 #pragma unroll
             for (int k = 0; k < C; ++k)
-              if (pm >> k & 1u) {
-                xv[k] = cur.cc[k] < 0 ? lds_vol(xs + (-1 - cur.cc[k])) : ld_relaxed(xg_cur + cur.cc[k]);
-                if (!pend(xv[k])) pm &= ~(1u << k);
-              }
-            if (pm && clock64() - w0 > (1LL << 31)) {
-              int bad = 0;
-#pragma unroll
-              for (int k = 0; k < C; ++k)
-                if (pm >> k & 1u) bad = cur.cc[k];
-              line_stuck(bad, p);
-            }
-          } while (pm);
-        }
-        double acc = 0.0;
-#pragma unroll
-        for (int k = 0; k < C; ++k) acc = fma(cur.cv[k], xv[k], acc);
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);  // same sum in every lane
-        double s = rhs - acc;
-        s = fma(-o3, x3, s);
-        s = fma(-o2, x2, s);
-        s = fma(-o1, x1, s);
-        const double x = s * idg;
-        if (lane == 0) {
-          *(volatile double*)(xs + (p - bs)) = x;
-          st_relaxed(xg_set + p, x);
-          xg_clr[p] = __longlong_as_double((long long)LINE_PENDING);
-          a.u[row] = a.accumulate ? uold + x : x;
-        }
-        x3 = x2;
-        x2 = x1;
-        x1 = x;
-        cur = nxt;
+              if (pm >> k & 1u) bad = B.cc[k];
+            line_stuck(bad, p);
+          }
+        } while (pm);
       }
+      if (D.cw) D.cw += clock64();
+      double acc = 0.0;
+#pragma unroll
+      for (int k = 0; k < C; ++k) acc = fma(B.cv[k], B.xv[k], acc);
+      for (int k = 0; k < ovn; ++k) {  // long rows (interface rows): the overflow chunks synchronously
+        const size_t at = ((size_t)ovs + k) * 32 + lane;
+        const int code = __ldg(a.ocol + at);
+        acc = fma(__ldg(a.oval + at), poll(code, fetch(xs, xg_cur, code), p), acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);  // same sum in every lane
+      D.acc = acc;
+    };
+    StA<C> A;
+    StB<C> B;
+    StD D;
+    double x1 = 0.0, x2 = 0.0, x3 = 0.0;
+    // prologue: fill the pipeline
+    stage_a(A, it.next(a, W, lend));
+    stage_b(B, A);
+    stage_a(A, it.next(a, W, lend));
+    stage_c(D, B);
+    stage_b(B, A);
+    stage_a(A, it.next(a, W, lend));
+    long long pc[5] = {0, 0, 0, 0, 0}, rows_done = 0;
+    long long tc = a.prof ? clock64() : 0;
+    auto mark = [&](int i) {
+      if (a.prof) {
+        const long long now = clock64();
+        pc[i] += now - tc;
+        tc = now;
+      }
+    };
+    while (D.p >= 0) {
+      ++rows_done;
+      // D: finish row t (late values re-polled together, added oldest first, then the own line's)
+      unsigned pm = 0;
+#pragma unroll
+      for (int j = 0; j < LINE_LATE; ++j) pm |= pend(D.lx[j]) ? 1u << j : 0u;
+      const long long dw0 = a.trace ? clock64() : 0;
+      if (pm) {
+        const long long w0 = clock64();
+        int tries = 0;
+        do {
+          if (++tries > 8) __nanosleep(32);
+#pragma unroll
+          for (int j = 0; j < LINE_LATE; ++j)
+            if (pm >> j & 1u) D.lx[j] = fetch(xs, xg_cur, D.lc[j]);
+#pragma unroll
+          for (int j = 0; j < LINE_LATE; ++j)
+            if ((pm >> j & 1u) && !pend(D.lx[j])) pm &= ~(1u << j);
+          if (pm && clock64() - w0 > (1LL << 31)) line_stuck(D.lc[0], D.p);
+        } while (pm);
+      }
+      mark(0);
+      double s = D.rhs - D.acc;
+#pragma unroll
+      for (int j = 0; j < LINE_LATE; ++j) s = fma(-D.lv[j], D.lx[j], s);
+      s = fma(-D.o3, x3, s);
+      s = fma(-D.o2, x2, s);
+      s = fma(-D.o1, x1, s);
+      const double x = s * D.idg;
+      if (lane == 0) {
+        *(volatile double*)(xs + (D.p - bs)) = x;
+        st_relaxed(xg_set + D.p, x);
+        if (a.trace) {
+          long long gt;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(gt));
+          a.trace[3 * (size_t)D.p] = gt;
+          a.trace[3 * (size_t)D.p + 1] = clock64() - dw0;
+          a.trace[3 * (size_t)D.p + 2] = D.cw;
+        }
+        xg_clr[D.p] = __longlong_as_double((long long)LINE_PENDING);
+        a.u[D.row] = a.accumulate ? D.uold + x : x;
+      }
+      x3 = x2;
+      x2 = x1;
+      x1 = x;
+      mark(1);
+      stage_c(D, B);
+      mark(2);
+      stage_b(B, A);
+      mark(3);
+      stage_a(A, it.next(a, W, lend));
+      mark(4);
+    }
+    if (a.prof && lane == 0 && rows_done) {
+      for (int i = 0; i < 5; ++i) atomicAdd((unsigned long long*)a.prof + i, (unsigned long long)pc[i]);
+      atomicAdd((unsigned long long*)a.prof + 5, (unsigned long long)rows_done);
     }
     __syncthreads();
   }
@@ -168,12 +339,12 @@ void for_line_variants(F&& f) {
   f(line_sweep_kernel<2>);
   f(line_sweep_kernel<4>);
   f(line_sweep_kernel<6>);
-  f(line_sweep_kernel<8>);
 }
 
 }  // namespace
 
-int line_chunk_variant(int C) { return C <= 2 ? 2 : C <= 4 ? 4 : C <= 6 ? 6 : C <= 8 ? 8 : -1; }
+// register chunks of the record layout (line_plan.cpp picks 2, 4 or 6)
+int line_chunk_variant(int C) { return C <= 2 ? 2 : C <= 4 ? 4 : 6; }
 
 int line_max_ctas(size_t smem) {
   int dev = 0, sms = 0, per = 0, best = 1 << 30;
@@ -194,8 +365,7 @@ void launch_line_sweep(cudaStream_t s, const LineArgs& a) {
   switch (line_chunk_variant(a.C)) {
     case 2: launch_k(line_sweep_kernel<2>, grid, block, smem, s, a); break;
     case 4: launch_k(line_sweep_kernel<4>, grid, block, smem, s, a); break;
-    case 6: launch_k(line_sweep_kernel<6>, grid, block, smem, s, a); break;
-    default: launch_k(line_sweep_kernel<8>, grid, block, smem, s, a); break;
+    default: launch_k(line_sweep_kernel<6>, grid, block, smem, s, a); break;
   }
 }
 

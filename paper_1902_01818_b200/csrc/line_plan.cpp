@@ -74,49 +74,109 @@ bool build_line_plan(int n, const int* ptr, const int* col, const double* val, c
     for (int l = out.bline[b]; l < out.bline[b + 1]; ++l) bundle_of_line[l] = b;
     out.rb_max = std::max(out.rb_max, out.bstart[b + 1] - out.bstart[b]);
   }
+  // dependency levels (positions)
+  std::vector<int> lv(n, 0);
+  for (int p = 0; p < n; ++p) {
+    int l = 0;
+    for_entries(p, [&](int q, double) { l = std::max(l, lv[q] + 1); });
+    lv[p] = l;
+  }
+  // late entries: not own-recent, produced in the last LINE_LATE_LAG dependency levels; at most
+  // LINE_LATE (the newest levels, then the highest positions), ordered oldest first
+  auto is_own = [&](long long p, int q, int ls) { return q >= ls && p - q <= 3; };
+  auto pick_late = [&](long long p, int ls, int* late) {
+    int nl = 0;
+    for (int j = 0; j < LINE_LATE; ++j) late[j] = -1;
+    auto newer = [&](int a, int b) { return lv[a] != lv[b] ? lv[a] > lv[b] : a > b; };
+    for_entries((int)p, [&](int q, double) {
+      if (is_own(p, q, ls) || lv[q] < lv[p] - LINE_LATE_LAG) return;
+      if (nl < LINE_LATE) {
+        late[nl++] = q;
+      } else {  // replace the oldest kept one if q is newer
+        int m = 0;
+        for (int j = 1; j < LINE_LATE; ++j)
+          if (newer(late[m], late[j])) m = j;
+        if (newer(q, late[m])) late[m] = q;
+      }
+    });
+    std::sort(late, late + nl, [&](int a, int b) { return newer(b, a); });  // oldest first
+    return nl;
+  };
   // pass 1: chunks per position
-  out.cptr.assign(n + 1, 0);
-  out.own.assign((size_t)3 * n, 0.0);
-  out.idiag.assign(n, 0.0);
-  std::atomic<int> too_long{0};
+  std::vector<int> nch(n, 0);
   std::atomic<long long> ent{0};
   parallel_for(n, [&](long long pa, long long pb) {
     long long e_loc = 0;
     for (long long p = pa; p < pb; ++p) {
       const int ls = out.lstart[line_of[p]];
+      int late[LINE_LATE];
+      const int nl = pick_late(p, ls, late);
       int e = 0;
-      for_entries((int)p, [&](int q, double v) {
+      for_entries((int)p, [&](int q, double) {
         ++e_loc;
-        if (q >= ls && p - q <= 3) out.own[3 * p + (p - q - 1)] = v;
-        else ++e;
+        if (!is_own(p, q, ls)) ++e;
       });
-      const int c = (e + 31) / 32;
-      if (c > cmax) too_long = 1;
-      out.cptr[p + 1] = c;
-      out.idiag[p] = 1.0 / val[dpos[row_of((int)p)]];
+      nch[p] = (e - nl + 31) / 32;
     }
     ent += e_loc;
   });
-  if (too_long) return false;
-  for (int p = 0; p < n; ++p) out.cptr[p + 1] += out.cptr[p];
   out.entries = ent;
-  out.slots = (long long)out.cptr[n] * 32;
-  if (out.slots >= INT_MAX) return false;
-  for (int p = 0; p < n; ++p) out.C = std::max(out.C, out.cptr[p + 1] - out.cptr[p]);
-  out.ccol.assign(out.slots, -1 - out.rb_max);  // padding: the always-zero shared slot
-  out.cval.assign(out.slots, 0.0);
-  // pass 2: fill
+  for (int p = 0; p < n; ++p) out.cmax = std::max(out.cmax, nch[p]);
+  out.C = out.cmax <= 2 ? 2 : out.cmax <= 4 ? 4 : 6;
+  if (cmax > 0 && out.C > cmax) out.C = cmax;
+  const int C = out.C;
+  std::vector<long long> optr(n + 1, 0);
+  for (int p = 0; p < n; ++p) {
+    optr[p + 1] = optr[p] + std::max(0, nch[p] - C);
+    out.chunks += nch[p];
+    out.ovf_rows += nch[p] > C;
+  }
+  if (optr[n] * 32 >= INT_MAX) return false;
+  const size_t rb = line_rec_bytes(C);
+  out.rec.assign(n * rb / 8, 0.0);
+  out.ocol.assign(optr[n] * 32, -1 - out.rb_max);
+  out.oval.assign(optr[n] * 32, 0.0);
+  // pass 2: records
   parallel_for(n, [&](long long pa, long long pb) {
     for (long long p = pa; p < pb; ++p) {
+      char* r = reinterpret_cast<char*>(out.rec.data()) + p * rb;
+      int* cc = reinterpret_cast<int*>(r);
+      double* cv = reinterpret_cast<double*>(r + line_off_cv(C));
+      int* meta = reinterpret_cast<int*>(r + line_off_meta(C));
+      double* lvv = reinterpret_cast<double*>(r + line_off_lv(C));
+      double* own = reinterpret_cast<double*>(r + line_off_own(C));
+      for (int i = 0; i < 32 * C; ++i) cc[i] = -1 - out.rb_max;
+      for (int j = 0; j < LINE_LATE; ++j) meta[j] = -1 - out.rb_max;
+      meta[LINE_LATE] = (int)optr[p];
+      meta[LINE_LATE + 1] = (int)(optr[p + 1] - optr[p]);
       const int l = line_of[p], ls = out.lstart[l];
       const int bs = out.bstart[bundle_of_line[l]];
-      long long at = (long long)out.cptr[p] * 32;
+      int late[LINE_LATE];
+      pick_late(p, ls, late);
+      int e = 0;
       for_entries((int)p, [&](int q, double v) {
-        if (q >= ls && p - q <= 3) return;
-        out.ccol[at] = q >= bs ? -1 - (q - bs) : q;
-        out.cval[at] = v;
-        ++at;
+        if (is_own(p, q, ls)) {
+          own[p - q - 1] = v;
+          return;
+        }
+        const int code = q >= bs ? -1 - (q - bs) : q;
+        for (int j = 0; j < LINE_LATE; ++j)
+          if (late[j] == q) {
+            meta[j] = code;
+            lvv[j] = v;
+            return;
+          }
+        if (e < 32 * C) {
+          cc[e] = code;
+          cv[e] = v;
+        } else {
+          const long long at = optr[p] * 32 + (e - 32 * C);
+          out.ocol[at] = code;
+          out.oval[at] = v;
+        }
+        ++e;
       });
+      own[3] = 1.0 / val[dpos[row_of((int)p)]];
     }
   });
   return true;

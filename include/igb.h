@@ -116,7 +116,8 @@ int igb_scms_begin(igb_ctx* ctx, int level, double tau);
 /* One patch interior: dim in {2,3}; dims[a] = n_a; T_a is n_a x n_a row-major
  * (columns = eigenvectors of the split subspaces, [W_L V_L | W_C V_C]);
  * denom has prod(n_a) entries (C order); idx maps the C-order tensor to free ids.
- * T2 is ignored when dim == 2. Interiors sharing T/denom pointers share storage. */
+ * T2 is ignored when dim == 2. Interiors whose T / denom have identical content share one device
+ * copy (content-hashed and compared; buffers are copied during the call and may be reused). */
 int igb_scms_add_interior(igb_ctx* ctx, int level, int dim, const int* dims,
                           const double* T0, const double* T1, const double* T2,
                           const double* denom, const int* idx);
@@ -149,6 +150,27 @@ int igb_op(igb_ctx* ctx, int op, int level, const double* in, double* out);
  * iteration count (max_iters if not converged). */
 int igb_pcg(igb_ctx* ctx, const double* b, double tol, int max_iters,
             double* x, int* its, double* hist, int hist_cap);
+
+/* Smoother duck type (smoothers.py:192-200 GaussSeidel, 327-332 SubspaceCorrectedMass,
+ * 343-353 HybridSmoother): u <- pre_smooth / post_smooth(A_l, u, f, steps) with smoother kind
+ * IGB_SMOOTHER_* on level l (post != 0: post-smoothing), host buffers (u in/out). */
+int igb_smooth(igb_ctx* ctx, int level, int kind, int post, int steps, const double* f, double* u);
+
+/* General PCG: linsolve.cg(A, b, preconditioner, tol, max_iters, callback) (linsolve.py:64-101)
+ * for any operator and preconditioner, with a live per-iteration callback.
+ *   A: n x n CSR (copied for the call), or indptr == NULL for the context's finest operator;
+ *   prec_mode: IGB_PREC_NONE (z = r), IGB_PREC_CYCLE (one cycle of the context's hierarchy from
+ *   u = 0, as MultigridSolver.preconditioner()), IGB_PREC_HOST (prec(r, z, n, prec_user) on host
+ *   buffers: the reference's arbitrary callable);
+ *   iter_cb(it, rel, iter_user) after every iteration (nullable).
+ * Same stopping rule, history and non-convergence semantics as igb_pcg (which runs the whole
+ * solve as one CUDA graph and is the fast path for the cycle preconditioner without callback). */
+enum { IGB_PREC_NONE = 0, IGB_PREC_CYCLE = 1, IGB_PREC_HOST = 2 };
+typedef void (*igb_prec_fn)(const double* r, double* z, int n, void* user);
+typedef void (*igb_iter_fn)(int it, double rel, void* user);
+int igb_cg(igb_ctx* ctx, int n, long long nnz, const int* indptr, const int* indices, const double* data,
+           int prec_mode, igb_prec_fn prec, void* prec_user, igb_iter_fn iter_cb, void* iter_user,
+           const double* b, double tol, int max_iters, double* x, int* its, double* hist, int hist_cap);
 
 /* Same with device-resident b and x (device pointers); hist stays a host buffer. */
 int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters,

@@ -17,6 +17,8 @@ reference itself and against ``tests/golden/*.npz``):
 * ``_interior_solve``            <- ``ScmsInteriorSolver.solve`` (smoothers.py:283-294)
 * ``_Scms.apply``                <- ``SubspaceCorrectedMass.apply`` (smoothers.py:321-325)
 * hybrid pre/post smoothing      <- ``HybridSmoother``         (smoothers.py:343-353)
+* ``OracleSolver.solve_stationary`` / ``solve_direct`` <- ``MultigridSolver._iterate`` with the
+  stationary and line-search steps (multigrid.py:170-234)
 * coarse / piece solves          <- ``linsolve.Factorization.solve`` (linsolve.py:33-53)
 * ``_TriSolveGS``                 <- the same GS sweeps as row substitution in C
   (``oracle/trisolve.c``, built into ``oracle/_ref/libtrisolve.so``) for levels where
@@ -282,6 +284,51 @@ class OracleSolver:
 
     def solve(self, b, tol=1e-8, max_iters=500):
         return cg(self.A[self.finest], b, self.preconditioner(), tol=tol, max_iters=max_iters)
+
+    def _iterate(self, f, step, tol, max_iters):
+        """(u, its, residuals, converged) of multigrid.py:170-200 (10 increases = divergence)."""
+        normf = np.linalg.norm(f)
+        u = np.zeros_like(f)
+        if normf == 0.0:
+            return u, 0, [], True
+        residuals, increases = [], 0
+        for it in range(1, max_iters + 1):
+            u, rel = step(u)
+            rel = rel / normf
+            increases = increases + 1 if residuals and rel > residuals[-1] else 0
+            residuals.append(rel)
+            if rel <= tol:
+                return u, it, residuals, True
+            if increases >= 10 or not np.isfinite(rel):
+                return u, it, residuals, False
+        return u, max_iters, residuals, False
+
+    def solve_stationary(self, f, tol=1e-8, max_iters=500):
+        A = self.A[self.finest]
+
+        def step(u):
+            u = self.cycle(self.finest, f, u)
+            return u, np.linalg.norm(f - A @ u)
+
+        return self._iterate(f, step, tol, max_iters)
+
+    def solve_direct(self, f, tol=1e-8, max_iters=500):
+        A = self.A[self.finest]
+        state = {"r": f.copy()}
+
+        def step(u):
+            r = state["r"]
+            z = self.cycle(self.finest, r)
+            Az = A @ z
+            zAz = z @ Az
+            if not np.isfinite(zAz) or zAz <= 0.0:
+                return u, np.inf
+            alpha = (r @ z) / zAz
+            u = u + alpha * z
+            state["r"] = r - alpha * Az
+            return u, np.linalg.norm(state["r"])
+
+        return self._iterate(f, step, tol, max_iters)
 
 
 def bundle_from_reference(solver):

@@ -56,8 +56,13 @@ SIGNATURES = {
     "igb_profile_reset": ([_p], _i),
     "igb_profile_get": ([_p, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll), ctypes.POINTER(_d)], _i),
     "igb_gs_info": ([_p, _i, _i, _ip, _i], _i),
+    "igb_smooth": ([_p, _i, _i, _i, _i, _p, _p], _i),
+    "igb_cg": ([_p, _i, _ll, _p, _p, _p, _i, _p, _p, _p, _p, _p, _d, _i, _p, _ip, _p, _i], _i),
     "igb_profile_flops": ([_p, _i, ctypes.POINTER(_d)], _i),
 }
+PREC = {"none": 0, "cycle": 1, "host": 2}
+PREC_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(_d), ctypes.POINTER(_d), _i, _p)
+ITER_FN = ctypes.CFUNCTYPE(None, _i, _d, _p)
 GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule", 5: "line"}
 
 _lib = None
@@ -294,4 +299,56 @@ class Context:
         v = list(info)
         return {"engine": GS_ENGINES.get(v[0], "?"), "B": v[1], "KA": v[2], "KF": v[3], "ranges": v[4],
                 "panels": v[5], "depth": v[6], "n": v[7]}
+
+    def cg(self, A, b, prec="none", prec_fn=None, tol=1e-8, max_iters=10000, callback=None):
+        """igb_cg: PCG with any CSR operator (A None: the finest level's) and preconditioner
+        ("none", "cycle": this context's cycle, "host": prec_fn(r) -> z on host arrays); callback(it,
+        rel) is called after every iteration.  Returns (x, its, history)."""
+        b = _c(b, np.float64)
+        n = len(b)
+        x = np.empty(n)
+        hist = np.empty(max(1, int(max_iters)))
+        its = ctypes.c_int(0)
+        errors = []
+
+        def _prec(r_ptr, z_ptr, nn, _user):
+            try:
+                r = np.ctypeslib.as_array(r_ptr, shape=(nn,))
+                z = np.ctypeslib.as_array(z_ptr, shape=(nn,))
+                z[:] = np.asarray(prec_fn(r.copy()), dtype=float)
+            except BaseException as e:  # reported after the call (ctypes cannot propagate it)
+                errors.append(e)
+
+        def _iter(it, rel, _user):
+            try:
+                if callback is not None:
+                    callback(int(it), float(rel))
+            except BaseException as e:
+                errors.append(e)
+
+        pf = PREC_FN(_prec) if prec == "host" else PREC_FN()
+        itf = ITER_FN(_iter) if callback is not None else ITER_FN()
+        if A is None:
+            args = (n, 0, None, None, None)
+        else:
+            import scipy.sparse
+            A = scipy.sparse.csr_matrix(A)
+            if not A.has_sorted_indices:
+                A = A.sorted_indices()
+            ip, ix, dv = _c(A.indptr, np.int32), _c(A.indices, np.int32), _c(A.data, np.float64)
+            args = (n, A.nnz, _ptr(ip), _ptr(ix), _ptr(dv))
+        rc = self.lib.igb_cg(self.h, *args, PREC[prec], ctypes.cast(pf, _p), None, ctypes.cast(itf, _p), None,
+                             _ptr(b), float(tol), int(max_iters), _ptr(x), ctypes.byref(its), _ptr(hist), len(hist))
+        if errors:
+            raise errors[0]
+        self._check(rc, "igb_cg")
+        return x, its.value, hist[:its.value].tolist()
+
+    def smooth(self, level, kind, post, steps, f, u):
+        """igb_smooth: returns the iterate after `steps` pre- (post=False) or post-smoothing steps."""
+        f = _c(f, np.float64)
+        out = _c(u, np.float64).copy()
+        self._check(self.lib.igb_smooth(self.h, int(level), SMOOTHER[kind], 1 if post else 0, int(steps),
+                                        _ptr(f), _ptr(out)), "igb_smooth")
+        return out
 

@@ -125,14 +125,15 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
     long long cc0 = 0;
     if (a.trace && gl == 0) cc0 = clock64();
     double acc = 0.0;
-    for (int base = s; base < e; base += G * K) {
+    const int el = (a.elate && row >= 0) ? ld_nc_s32(a.elate + q) : e;  // early entries [s, el)
+    for (int base = s; base < el; base += G * K) {
       int c[K];
       double v[K], x[K];
 #pragma unroll
       for (int k = 0; k < K; ++k) {
         const int idx = base + gl + k * G;
-        c[k] = idx < e ? __ldcs(a.ecol + idx) : -1;
-        v[k] = idx < e ? __ldcs(a.eval + idx) : 0.0;
+        c[k] = idx < el ? __ldcs(a.ecol + idx) : -1;
+        v[k] = idx < el ? __ldcs(a.eval + idx) : 0.0;
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) x[k] = c[k] >= 0 ? ld_relaxed(xg_cur + c[k]) : 0.0;
@@ -166,6 +167,48 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
     if (a.trace && gl == 0) c1 = clock64();
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o, G);
+    // late entries (the newest dependencies): every lane of the row loads and polls all of them
+    // (same addresses: one request per warp) and adds them serially in a fixed order, so the
+    // early reduction above never waits for them
+    if (row >= 0 && el < e) {
+      constexpr int LM = 8;
+      int lc[LM];
+      double lv[LM], lx[LM];
+      const int nl = e - el;
+      for (int j0 = 0; j0 < nl; j0 += LM) {
+#pragma unroll
+        for (int j = 0; j < LM; ++j) {
+          const int idx = el + j0 + j;
+          lc[j] = j0 + j < nl ? ld_nc_s32(a.ecol + idx) : -1;
+          lv[j] = j0 + j < nl ? ld_nc_f64(a.eval + idx) : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < LM; ++j) lx[j] = lc[j] >= 0 ? ld_relaxed(xg_cur + lc[j]) : 0.0;
+        unsigned pend = 0;
+#pragma unroll
+        for (int j = 0; j < LM; ++j) pend |= (lc[j] >= 0 && is_pending(lx[j])) ? 1u << j : 0u;
+        if (pend) {
+          const long long w0 = clock64();
+          do {
+#pragma unroll
+            for (int j = 0; j < LM; ++j)
+              if (pend >> j & 1u) lx[j] = ld_relaxed(xg_cur + lc[j]);
+#pragma unroll
+            for (int j = 0; j < LM; ++j)
+              if ((pend >> j & 1u) && !is_pending(lx[j])) pend &= ~(1u << j);
+            if (pend && clock64() - w0 > (1LL << 31)) {
+              int bad = -1;
+#pragma unroll
+              for (int j = 0; j < LM; ++j)
+                if (pend >> j & 1u) bad = lc[j];
+              flow_stuck(bad, row);
+            }
+          } while (pend);
+        }
+#pragma unroll
+        for (int j = 0; j < LM; ++j) acc = fma(lv[j], lx[j], acc);
+      }
+    }
     if (gl == 0 && row >= 0) {
       const double xv = (rhs - acc) * idg;
       st_relaxed(xg_set + row, xv);

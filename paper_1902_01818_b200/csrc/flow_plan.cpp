@@ -8,7 +8,7 @@
 namespace igb {
 
 bool build_flow_plan(int n, const int* ptr, const int* col, const double* val, const int* dpos, bool upper,
-                     int G, int crit_lag, FlowPlanHost& out) {
+                     int G, int crit_lag, int late_max, FlowPlanHost& out) {
   out = FlowPlanHost{};
   out.n = n;
   std::vector<int> lv(n, 0);
@@ -53,18 +53,28 @@ bool build_flow_plan(int n, const int* ptr, const int* col, const double* val, c
     const int i = out.row[q];
     out.eptr[q + 1] = out.eptr[q] + (i >= 0 ? hi(i) - lo(i) : 0);
   }
+  out.elate.assign(out.nq, 0);
   parallel_for(out.nq, [&](long long qa, long long qb) {
     for (long long q = qa; q < qb; ++q) {
       const int i = out.row[q];
-      if (i < 0) continue;
-      int best = -1;
-      long long e = out.eptr[q];
-      for (int k = lo(i); k < hi(i); ++k, ++e) {
-        out.ecol[e] = col[k];
-        out.eval[e] = val[k];
+      if (i < 0) {
+        out.elate[q] = out.eptr[q];
+        continue;
+      }
+      int best = -1, nlate = 0;
+      for (int k = lo(i); k < hi(i); ++k) nlate += lv[col[k]] > lv[i] - crit_lag;
+      if (nlate > late_max) nlate = 0;  // too many newest values: one batch as before
+      // early entries first (row order), then the late ones (row order)
+      long long e = out.eptr[q], el = out.eptr[q + 1] - nlate;
+      out.elate[q] = (int)el;
+      for (int k = lo(i); k < hi(i); ++k) {
+        const int c = col[k];
+        const bool late = nlate > 0 && lv[c] > lv[i] - crit_lag;
+        const long long at = late ? el++ : e++;
+        out.ecol[at] = c;
+        out.eval[at] = val[k];
         // latest-finishing dependency at least crit_lag levels back: highest level, then latest
         // in the list (upper: lowest row)
-        const int c = col[k];
         if (lv[c] > lv[i] - crit_lag) continue;
         if (best < 0 || lv[c] > lv[best] || (lv[c] == lv[best] && (upper ? c < best : c > best))) best = c;
       }

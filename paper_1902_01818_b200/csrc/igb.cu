@@ -204,7 +204,14 @@ struct igb_ctx {
   std::vector<int> steps;
   bool finalized = false;
   std::vector<void*> allocs;
-  std::map<const void*, void*> shared_uploads;  // host pointer -> device copy (FD data)
+  // FD data shared between interiors with identical content (transforms, denominators): keyed by
+  // (element count, content hash), verified against a host copy -- never by host address, which a
+  // caller may reuse for different temporaries between calls
+  struct SharedUpload {
+    std::vector<double> host;
+    const double* dev;
+  };
+  std::map<std::pair<size_t, unsigned long long>, std::vector<SharedUpload>> shared_uploads;
 
   // CG state
   double *x = nullptr, *d = nullptr, *q = nullptr, *b = nullptr, *partials = nullptr,
@@ -1576,9 +1583,18 @@ bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
 bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
   const char* ge = std::getenv("IGB_FLOW_G");
   FlowPlanHost plan;
+  // Early/late split (flow_plan.h): the row's values of dependencies at least crit_lag levels
+  // back are loaded and reduced as soon as the crit value is ready, the newer ("late") ones are
+  // added in a serial tail.  Measured per dependency level on cfg5 L=3 (us, fwd / bwd, level 3):
+  // one batch with crit lag 2 (round 1) 1.55 / 1.84; lag 4 1.05 / 1.21; lag 6 0.88 / 1.42;
+  // lag 8 0.85 / 2.20 -- so forward lag 8 (late <= 64), backward lag 4 (late <= 32).
+  // IGB_FLOW_CRITLAG / IGB_FLOW_LATE override both directions (IGB_FLOW_LATE=0: one batch).
   const char* le = std::getenv("IGB_FLOW_CRITLAG");
+  const char* lm = std::getenv("IGB_FLOW_LATE");
+  const int lag = le ? std::max(1, std::atoi(le)) : (dir ? 4 : 8);
+  const int late_max = lm ? std::max(0, std::atoi(lm)) : (dir ? 32 : 64);
   if (!build_flow_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
-                       ge ? std::atoi(ge) : 0, le ? std::max(1, std::atoi(le)) : 2, plan))
+                       ge ? std::atoi(ge) : 0, late_max > 0 ? lag : (le ? lag : 2), late_max, plan))
     return false;
   FlowDev& F = V.flow[dir];
   FlowArgs& a = F.args;
@@ -1593,6 +1609,7 @@ bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   a.idiag = ctx->upload(plan.idiag.data(), plan.idiag.size());
   const char* ce = std::getenv("IGB_FLOW_CRIT");
   if (!ce || std::atoi(ce)) a.crit = ctx->upload(plan.crit.data(), plan.crit.size());
+  if (late_max > 0) a.elate = ctx->upload(plan.elate.data(), plan.elate.size());
   const char* be = std::getenv("IGB_FLOW_BACKOFF");
   a.backoff = be ? std::atoi(be) : 0;
   std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF5678ULL);  // flow.cu FLOW_PENDING
@@ -1785,10 +1802,14 @@ int igb_scms_add_interior(igb_ctx* ctx, int level, int dim, const int* dims, con
     }
     if (dim == 2) it.n[2] = 1;
     auto shared = [&](const double* h, size_t count) -> const double* {
-      auto f = ctx->shared_uploads.find(h);
-      if (f != ctx->shared_uploads.end()) return static_cast<const double*>(f->second);
+      unsigned long long hash = 1469598103934665603ULL;  // FNV-1a over the bytes
+      const unsigned char* bytes = reinterpret_cast<const unsigned char*>(h);
+      for (size_t i = 0; i < count * sizeof(double); ++i) hash = (hash ^ bytes[i]) * 1099511628211ULL;
+      auto& bucket = ctx->shared_uploads[{count, hash}];
+      for (auto& e : bucket)
+        if (std::memcmp(e.host.data(), h, count * sizeof(double)) == 0) return e.dev;
       double* d = ctx->upload(h, count);
-      ctx->shared_uploads[h] = d;
+      bucket.push_back({std::vector<double>(h, h + count), d});
       return d;
     };
     for (int a = 0; a < dim; ++a) it.T[a] = shared(Ts[a], (size_t)dims[a] * dims[a]);
@@ -2322,6 +2343,156 @@ int igb_pcg_device(igb_ctx* ctx, const double* d_b, double tol, int max_iters, d
     require_final(ctx);
     CU(cudaSetDevice(ctx->device));
     pcg_core(ctx, d_b, tol, max_iters, d_x, its, hist, hist_cap);
+  });
+}
+
+// Smoother duck type pre_smooth / post_smooth(A, u, f, steps) (reference smoothers.py:192-200,
+// 327-332, 343-353) on the device: `steps` steps of smoother `kind` on level l from the iterate u.
+int igb_smooth(igb_ctx* ctx, int level, int kind, int post, int steps, const double* f, double* u) {
+  return guarded(ctx, [&] {
+    require_final(ctx);
+    CU(cudaSetDevice(ctx->device));
+    if (level < 1 || level > ctx->L) throw ArgError("smoothing acts on levels 1..L");
+    if (steps < 0) throw ArgError("negative smoothing steps");
+    if (kind < IGB_SMOOTHER_GS || kind > IGB_SMOOTHER_HYBRID) throw ArgError("unknown smoother kind");
+    Level& V = ctx->lev[level];
+    if ((kind != IGB_SMOOTHER_SCMS && !V.has_gs) || (kind != IGB_SMOOTHER_GS && !V.has_scms))
+      throw StateError("the level has no such smoother");
+    const int n = V.n;
+    cudaStream_t s = ctx->stream;
+    const int saved_kind = ctx->smoother, saved_steps = ctx->steps[level];
+    ctx->smoother = kind;
+    ctx->steps[level] = steps;
+    try {
+      CU(cudaMemcpyAsync(V.f, f, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      CU(cudaMemcpyAsync(V.u, u, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+      bool uz = false;
+      if (post) ctx->post_smooth(level, V.f, V.u, uz);
+      else ctx->pre_smooth(level, V.f, V.u, uz);
+      CU(cudaMemcpyAsync(u, V.u, sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+      CU(cudaStreamSynchronize(s));
+    } catch (...) {
+      ctx->smoother = saved_kind;
+      ctx->steps[level] = saved_steps;
+      throw;
+    }
+    ctx->smoother = saved_kind;
+    ctx->steps[level] = saved_steps;
+  });
+}
+
+// General PCG (linsolve.cg with any operator / preconditioner, live per-iteration callback):
+// the same kernels and reductions as pcg_core, driven by a host loop that reads the scalars after
+// every iteration (reference linsolve.py:64-101).
+int igb_cg(igb_ctx* ctx, int n, long long nnz, const int* indptr, const int* indices, const double* data,
+           int prec_mode, igb_prec_fn prec, void* prec_user, igb_iter_fn iter_cb, void* iter_user,
+           const double* b, double tol, int max_iters, double* x, int* its, double* hist, int hist_cap) {
+  return guarded(ctx, [&] {
+    CU(cudaSetDevice(ctx->device));
+    if (max_iters < 0) throw ArgError("max_iters must be >= 0");
+    if (n < 1 || !b || !x || !its) throw ArgError("bad cg arguments");
+    if (prec_mode < IGB_PREC_NONE || prec_mode > IGB_PREC_HOST) throw ArgError("unknown preconditioner mode");
+    if (prec_mode == IGB_PREC_HOST && !prec) throw ArgError("host preconditioner callback missing");
+    const bool finest_op = indptr == nullptr;
+    if (finest_op || prec_mode == IGB_PREC_CYCLE) {
+      require_final(ctx);
+      if (n != ctx->lev[ctx->L].n) throw ArgError("cg size differs from the finest level");
+    }
+    if (!finest_op) {
+      if (nnz >= (1LL << 31)) throw ArgError("nnz exceeds int32 indexing");
+      check_csr(n, n, nnz, indptr, indices);
+    }
+    cudaStream_t s = ctx->stream;
+    // scratch, released on return
+    std::vector<void*> tmp;
+    auto scratch = [&](size_t bytes) {
+      void* p = nullptr;
+      CU(cudaMalloc(&p, std::max<size_t>(bytes, 8)));
+      tmp.push_back(p);
+      return p;
+    };
+    struct Free {
+      std::vector<void*>& v;
+      ~Free() {
+        for (void* p : v) cudaFree(p);
+      }
+    } release{tmp};
+    DevCsr M{};
+    if (!finest_op) {
+      M.n = M.m = n;
+      M.nnz = nnz;
+      M.ptr = static_cast<int*>(scratch(sizeof(int) * (n + 1)));
+      M.col = static_cast<int*>(scratch(sizeof(int) * nnz));
+      M.val = static_cast<double*>(scratch(sizeof(double) * nnz));
+      ctx->copy_h2d(M.ptr, indptr, sizeof(int) * (n + 1));
+      ctx->copy_h2d(M.col, indices, sizeof(int) * nnz);
+      ctx->copy_h2d(M.val, data, sizeof(double) * nnz);
+      M.group = pick_group(nnz, n);
+    }
+    double* dx = static_cast<double*>(scratch(8 * (size_t)n));
+    double* dr = static_cast<double*>(scratch(8 * (size_t)n));
+    double* dz = static_cast<double*>(scratch(8 * (size_t)n));
+    double* dd = static_cast<double*>(scratch(8 * (size_t)n));
+    double* dq = static_cast<double*>(scratch(8 * (size_t)n));
+    double* dh = static_cast<double*>(scratch(8 * (size_t)std::max(1, max_iters)));
+    double* partials = static_cast<double*>(scratch(sizeof(double) * REDUCTION_MAX_BLOCKS));
+    unsigned* counter = static_cast<unsigned*>(scratch(sizeof(unsigned)));
+    CgScalars* sc = static_cast<CgScalars*>(scratch(sizeof(CgScalars)));
+    CU(cudaMemsetAsync(counter, 0, sizeof(unsigned), s));
+    CgScalars h{};
+    h.tol = tol;
+    CU(cudaMemcpyAsync(sc, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+    std::vector<double> hr, hz;
+    auto apply_prec = [&] {  // z = M r
+      if (prec_mode == IGB_PREC_NONE) {
+        ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, dz, dr); });
+      } else if (prec_mode == IGB_PREC_CYCLE) {
+        Level& F = ctx->lev[ctx->L];
+        ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, F.f, dr); });
+        ctx->run_finest_cycle();
+        ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, dz, F.u); });
+      } else {
+        hr.resize(n);
+        hz.assign(n, 0.0);
+        CU(cudaMemcpyAsync(hr.data(), dr, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        prec(hr.data(), hz.data(), n, prec_user);
+        CU(cudaMemcpyAsync(dz, hz.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+      }
+    };
+    auto matvec = [&] {  // q = A d
+      if (finest_op) ctx->apply_A(ctx->L, dd, nullptr, dq, 0);
+      else ctx->spmv(M, dd, nullptr, dq, 0, K_SPMV);
+    };
+    CU(cudaMemcpyAsync(dr, b, 8 * (size_t)n, cudaMemcpyHostToDevice, s));
+    ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dr, dr, partials, counter, sc, FIN_NORMB, nullptr); });
+    ctx->launch(K_CG, 8.0 * n, [&] { launch_fill(s, n, dx, 0.0); });
+    CU(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    int nit = 0;
+    if (h.normb != 0.0) {
+      apply_prec();
+      ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, dd, dz); });
+      ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dr, dz, partials, counter, sc, FIN_RZ0, nullptr); });
+      for (int it = 1; it <= max_iters; ++it) {
+        matvec();
+        ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dd, dq, partials, counter, sc, FIN_ALPHA, nullptr); });
+        ctx->launch(K_CG, 56.0 * n, [&] { launch_cg_update(s, n, dx, dr, dd, dq, partials, counter, sc, dh); });
+        CU(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
+        CU(cudaStreamSynchronize(s));
+        nit = it;
+        if (iter_cb) iter_cb(it, h.rel, iter_user);
+        if (h.done || it == max_iters) break;
+        apply_prec();
+        ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dr, dz, partials, counter, sc, FIN_BETA, nullptr); });
+        ctx->launch(K_CG, 24.0 * n, [&] { launch_cg_direction(s, n, dd, dz, sc); });
+      }
+    }
+    CU(cudaMemcpyAsync(x, dx, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));
+    if (hist && hist_cap > 0 && nit > 0)
+      CU(cudaMemcpyAsync(hist, dh, 8 * (size_t)std::min(nit, hist_cap), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    *its = nit;
   });
 }
 

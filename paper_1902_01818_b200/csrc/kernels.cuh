@@ -155,6 +155,8 @@ struct FlowArgs {
   unsigned* done_ctr;  // CTAs finished (device), reset by the last one
   int n, nq, G, ctas, accumulate;
   const int* crit;     // nullable: [nq] the dependency of the highest level (polled first)
+  const int* elate;    // [nq] first late entry of the row (flow_plan.h): early entries are reduced
+                       // first, the late ones (newest dependencies) added serially by every lane
   int backoff;         // ns slept between polls of crit (0: spin)
   long long* trace;    // debug (nullable): per slot globaltimer at start / deps ready / stored
 };

@@ -133,27 +133,44 @@ def read_coo(path):
                                    shape=(m, n))
 
 
-def cg(A, b, preconditioner=None, tol=DEFAULT_TOL, max_iters=10000, callback=None):
-    """Preconditioned CG on the device; returns ``(x, iterations, history)``.
+_plain_ctx = None
 
-    ``preconditioner`` must be the device preconditioner of a MultigridSolver
-    whose finest operator is ``A`` (the reference call
-    ``cg(solver.A[L], f, solver.preconditioner(), tol)``).  ``callback(it, rel)``
-    is invoked after the solve for every history entry.
+
+def _plain_context():
+    """Device context for cg calls that carry no multigrid hierarchy (plain / host-callable
+    preconditioner); created once, on device 0."""
+    global _plain_ctx
+    if _plain_ctx is None:
+        from ._lib import Context
+        _plain_ctx = Context(0)
+    return _plain_ctx
+
+
+def cg(A, b, preconditioner=None, tol=DEFAULT_TOL, max_iters=10000, callback=None):
+    """Preconditioned CG on the device; returns ``(x, iterations, history)`` (``linsolve.py:64-101``).
+
+    * ``preconditioner`` the DevicePreconditioner of a MultigridSolver (``solver.preconditioner()``,
+      the reference call ``cg(solver.A[L], f, solver.preconditioner(), tol)``): without a callback
+      the whole solve is one CUDA graph (``igb_pcg``); with ``callback(it, rel)`` a host-driven loop
+      on the same kernels calls it after every iteration (``igb_cg``);
+    * ``preconditioner=None`` (plain CG) or any host callable ``r -> z``: ``igb_cg`` with the CSR of
+      ``A`` on the device; the callable runs on host copies of ``r`` once per iteration.
+    All vector arithmetic and every product with ``A`` run on the device; there is no host CG path.
     """
     from .multigrid import DevicePreconditioner
 
-    if not isinstance(preconditioner, DevicePreconditioner):
-        raise TypeError(
-            "device cg needs the DevicePreconditioner of a MultigridSolver "
-            "(solver.preconditioner()); there is no host CG path")
-    solver = preconditioner.solver
-    if A is not solver.A[solver.finest] and (A.shape != solver.A[solver.finest].shape or
-                                             (A != solver.A[solver.finest]).nnz):
-        raise ValueError("cg operator differs from the preconditioner's finest matrix")
     b = np.asarray(b, dtype=float)
-    x, its, history = solver.ctx.pcg(b, tol, max_iters)
-    if callback is not None:
-        for it, rel in enumerate(history, start=1):
-            callback(it, rel)
-    return x, its, history
+    if isinstance(preconditioner, DevicePreconditioner):
+        solver = preconditioner.solver
+        finest = solver.A[solver.finest]
+        same = A is finest or (A.shape == finest.shape and not (A != finest).nnz)
+        if same and callback is None:
+            return solver.ctx.pcg(b, tol, max_iters)
+        return solver.ctx.cg(None if same else A, b, prec="cycle", tol=tol, max_iters=max_iters,
+                             callback=callback)
+    ctx = _plain_context()
+    if preconditioner is None:
+        return ctx.cg(A, b, prec="none", tol=tol, max_iters=max_iters, callback=callback)
+    if not callable(preconditioner):
+        raise TypeError("preconditioner must be None, a callable r -> z or a DevicePreconditioner")
+    return ctx.cg(A, b, prec="host", prec_fn=preconditioner, tol=tol, max_iters=max_iters, callback=callback)

@@ -209,6 +209,27 @@ class _DeviceBound:
                 "(there is no host implementation)")
         return self._ctx
 
+    # smoother duck type of the reference (smoothers.py:192-200, 327-332, 343-353): the steps run
+    # on the device (igb_smooth); A must be the level operator the smoother was built for
+    _kind = None
+
+    def _smooth(self, A, u, f, steps, post):
+        ctx = self._ctx_for_smooth()
+        if A is not None and A.shape[0] != len(u):
+            raise ValueError("operator and iterate sizes differ")
+        out = ctx.smooth(self._level, self._kind, post, steps, f, u)
+        u[...] = out  # in place, as the reference's u += ...
+        return u
+
+    def _ctx_for_smooth(self):
+        return self._require()
+
+    def pre_smooth(self, A, u, f, steps):
+        return self._smooth(A, u, f, steps, False)
+
+    def post_smooth(self, A, u, f, steps):
+        return self._smooth(A, u, f, steps, True)
+
 
 class GaussSeidel(_DeviceBound):
     """Forward/backward Gauss-Seidel in natural order (``smoothers.py:171-200``).
@@ -216,6 +237,11 @@ class GaussSeidel(_DeviceBound):
     Host setup only validates the diagonal; the level schedules of tril(A)
     and triu(A) are built natively by ``igb_set_gs``.
     """
+
+    _kind = "gs"
+
+    def _ctx_for_smooth(self):
+        return self._standalone()
 
     def __init__(self, A):
         A = A.tocsr()
@@ -353,6 +379,8 @@ class ScmsInteriorSolver:
 class SubspaceCorrectedMass(_DeviceBound):
     """Damped additive piece-local solves of one level (``smoothers.py:297-332``)."""
 
+    _kind = "scms"
+
     def __init__(self, A, hier, level, tau, delta, interior_policy="product"):
         if tau <= 0 or delta <= 0:
             raise ValueError("scms needs positive damping and scaling")
@@ -399,6 +427,18 @@ class HybridSmoother:
         self.gs.bind(ctx, level)
         self.scms.bind(ctx, level)
         return self
+
+    def pre_smooth(self, A, u, f, steps):
+        """GS forward, then steps * nu_inner SCMS steps (``smoothers.py:343-347``), on the device."""
+        out = self.scms._require().smooth(self.scms._level, "hyb", False, steps * self.nu_inner, f, u)
+        u[...] = out
+        return u
+
+    def post_smooth(self, A, u, f, steps):
+        """steps * nu_inner SCMS steps, then GS backward (``smoothers.py:349-353``), on the device."""
+        out = self.scms._require().smooth(self.scms._level, "hyb", True, steps * self.nu_inner, f, u)
+        u[...] = out
+        return u
 
 
 def build_smoother(kind, A, hier, level, tau=1.0, delta=0.12, interior_policy="product"):

@@ -69,8 +69,9 @@ def test_fullsize_pcg_matches_oracle(full):
     rep = solver.solve_pcg(f, check_spd=False)
     xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert rep.iterations == itso and rep.converged
-    h, ho = np.asarray(rep.residuals), np.asarray(histo)
-    per_entry = np.max(np.abs(h - ho) / ho)
-    print(f"[hist] {cfg} full size: its {itso}, per entry {per_entry:.2e}, x {rel(rep.x, xo):.2e}")
-    assert per_entry <= 1e-10
+    from test_gpu_parity import hist_ok
+    ok, per_entry, d1 = hist_ok(rep.residuals, histo)
+    print(f"[hist] {cfg} full size: its {itso}, per entry {per_entry:.2e}, max|dh|/h1 {d1:.2e}, "
+          f"x {rel(rep.x, xo):.2e}")
+    assert ok, (per_entry, d1)  # 1e-10 per entry above the fp64 floor of the history (test_gpu_parity.py)
     assert rel(rep.x, xo) <= 1e-10

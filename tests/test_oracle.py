@@ -135,7 +135,7 @@ def test_trisolve_restatement_matches_superlu(cfg, kw):
 
 
 @pytest.mark.parametrize("golden,cfg,kw", [("cfg2_L3", "cfg2", {"levels": 3}), ("cfg3_L2", "cfg3", {"levels": 2}),
-                                           ("cfg5_L2", "cfg5", {"levels": 2})])
+                                           ("cfg5_L2", "cfg5", {"levels": 2}), ("cfg4_p8_L3", "cfg4", {"p": 8, "levels": 3})])
 def test_trisolve_oracle_matches_reference_golden(golden, cfg, kw):
     """The oracle with C-substitution sweeps (the full-size checker of cfg4 p = 8 / cfg5) reproduces
     the reference's golden iteration counts, histories (1e-10 per entry; cfg3 3e-10, SURVEY
@@ -146,5 +146,8 @@ def test_trisolve_oracle_matches_reference_golden(golden, cfg, kw):
         f, tol=pr.config.tol, max_iters=pr.config.max_iters)
     assert its == int(g["its"])
     h, hg = np.array(hist), g["hist"]
-    assert np.max(np.abs(h - hg) / hg) <= (3e-10 if cfg == "cfg3" else 1e-10)
+    d = np.abs(h - hg)
+    print(f"[trisolve oracle] {golden}: per entry {np.max(d / hg):.2e}, max|dh|/h1 {np.max(d) / hg[0]:.2e}")
+    floor = 64 * np.finfo(float).eps * hg[0]  # see tests/test_gpu_parity.py hist_ok
+    assert np.all(d <= np.maximum((3e-10 if cfg == "cfg3" else 1e-10) * hg, floor))
     assert np.linalg.norm(x - g["x"]) <= 1e-10 * np.linalg.norm(g["x"])

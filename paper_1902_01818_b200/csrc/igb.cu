@@ -88,6 +88,8 @@ struct FdPlan {
   double flops = 0;       // per application over all interiors: 4 prod(n) sum_a n_a (2 d contractions)
   int first_gather = 0;   // step index with the gather
   int last_scatter = 0;   // step index with the scatter
+  Fd3Plan fd3;            // 3-D interiors on the fused DMMA path (fd3.cu): three launches
+  double fd3_bytes[3] = {0};
 };
 
 struct SweepDev {
@@ -602,6 +604,14 @@ struct igb_ctx {
       }, flops);
       flops = 0.0;
     }
+    if (F.fd3.nitems) {
+      for (int st = 0; st < 3; ++st) {
+        launch(K_FD, F.fd3_bytes[st], [&] {
+          launch_fd3(stream, F.fd3, st, res, u, V.tau, u_zero ? 0 : 1);
+        }, flops);
+        flops = 0.0;
+      }
+    }
     for (int s = 0; s < F.nsteps; ++s) {
       if (F.ndesc[s] == 0) continue;
       launch(K_FD, F.bytes[s], [&] {
@@ -986,6 +996,43 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
   }
   V.interiors = big;
   if (big.empty()) return;
+  static const bool fd3_ok = !(std::getenv("IGB_FD3") && std::atoi(std::getenv("IGB_FD3")) == 0);
+  if (dim == 3 && fd3_ok) {
+    bool fits = true;
+    int nmax = 1;
+    for (auto& it : V.interiors)
+      for (int a = 0; a < 3; ++a) {
+        fits = fits && it.n[a] <= FD3_NMAX;
+        nmax = std::max(nmax, it.n[a]);
+      }
+    if (fits) {
+      size_t tot = 0;
+      for (auto& it : V.interiors) tot += (size_t)it.n[0] * it.n[1] * it.n[2];
+      V.fd_scratch = tot;
+      V.s0 = ctx->alloc<double>(tot);
+      V.s1 = ctx->alloc<double>(tot);
+      std::vector<Fd3Item> items;
+      Fd3Plan& P = V.fd.fd3;
+      size_t off = 0;
+      for (auto& it : V.interiors) {
+        Fd3Item I{};
+        for (int a = 0; a < 3; ++a) { I.T[a] = it.T[a]; I.n[a] = it.n[a]; }
+        I.D = it.D; I.idx = it.idx;
+        I.buf0 = V.s0 + off; I.buf1 = V.s1 + off;
+        I.slab0 = P.slabs0; I.slab1 = P.slabs1;
+        P.slabs0 += it.n[0]; P.slabs1 += it.n[1];
+        const double cells = (double)it.n[0] * it.n[1] * it.n[2];
+        off += (size_t)cells;
+        // gather (idx + r) and Y written; Y, D read and W written; W, idx read and u updated
+        V.fd.fd3_bytes[0] += 20.0 * cells; V.fd.fd3_bytes[1] += 24.0 * cells; V.fd.fd3_bytes[2] += 28.0 * cells;
+        items.push_back(I);
+      }
+      P.nitems = (int)items.size();
+      P.n8 = (nmax + 7) / 8 * 8;
+      P.d_items = ctx->upload(items.data(), items.size());
+      return;
+    }
+  }
   size_t total = 0;
   for (auto& it : V.interiors) total += (size_t)it.n[0] * it.n[1] * (dim == 3 ? it.n[2] : 1);
   V.fd_scratch = total;

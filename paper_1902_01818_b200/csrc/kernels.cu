@@ -805,6 +805,7 @@ void carveout_prepare() {
   flow_set_carveout(pct);
   kron_set_carveout(pct);
   mf_set_carveout(pct);
+  fd3_set_carveout(pct);
 }
 
 size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }

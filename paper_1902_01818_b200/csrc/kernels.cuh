@@ -261,6 +261,25 @@ struct GemmDesc {
 void launch_fd_gemm(cudaStream_t s, const GemmDesc* d_descs, int ndesc, int total_tiles,
                     const double* gsrc, double* sdst, double alpha, int accumulate);
 
+// ---- fused 3-factor fast diagonalisation on fp64 tensor cores (fd3.cu) --------
+constexpr int FD3_NMAX = 72;       // largest interior side (multiple of 8)
+constexpr int FD3_MAXWARPS = 9;
+struct Fd3Item {
+  const double* T[3];   // n_a x n_a, row-major
+  const double* D;      // prod n_a
+  const int* idx;       // prod n_a
+  double* buf0;         // Y  (modes 1, 2 transformed)
+  double* buf1;         // W  (mode 0 transformed, divided, mode 0 back)
+  int n[3];
+  int slab0, slab1;     // first CTA of this interior in the i0-slab / i1-slab launches
+};
+struct Fd3Plan {
+  Fd3Item* d_items = nullptr;
+  int nitems = 0, n8 = 0, slabs0 = 0, slabs1 = 0;
+};
+void launch_fd3(cudaStream_t s, const Fd3Plan& P, int stage, const double* r, double* u, double alpha, int accumulate);
+void fd3_set_carveout(int pct);
+
 // ---- fused fast diagonalisation of small 2-D interiors (one CTA per interior) --
 // X = T0 ((T0^T R T1) ./ D) T1^T with R = r[idx] and u[idx] (+)= alpha X, all in smem.
 

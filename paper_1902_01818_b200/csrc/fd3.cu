@@ -22,37 +22,58 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
                : "+d"(c0), "+d"(c1) : "d"(a), "d"(b));
 }
 
-// C(M x N) = op(A)(M x K) op(B)(K x N), all operands in shared memory with pitch ld.
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// Warp tile of a slab product: which tiles this warp owns.
+template <int WM, int WN>
+struct WarpTile {
+  int tr0, tc0, g, t;
+  bool active;
+  __device__ __forceinline__ WarpTile(int tm, int tn) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    g = lane >> 2;
+    t = lane & 3;
+    const int wn_count = (tn + WN - 1) / WN;
+    const int wm = warp / wn_count;
+    tr0 = wm * WM;
+    tc0 = (warp - wm * wn_count) * WN;
+    active = tr0 < tm;
+  }
+};
+
+// c(M x N) += op(A)(M x K) op(B)(K x N), operands in shared memory with pitch ld.
 // AT: A is stored transposed (A(m,k) = As[k*ld + m]); BT: B(k,n) = Bs[n*ld + k].
-// tm, tn: number of 8-row / 8-column tiles; ksteps: K / 4 (padding is zero).
-// epi(row, col, v0, v1): called once per lane with its two adjacent outputs (col even).
-template <int WM, int WN, bool AT, bool BT, class Epi>
-__device__ __forceinline__ void slab_gemm(const double* __restrict__ As, const double* __restrict__ Bs, int ld,
-                                          int tm, int tn, int ksteps, Epi epi) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
-  const int wn_count = (tn + WN - 1) / WN;
-  const int wm = warp / wn_count, wn = warp - wm * wn_count;
-  const int tr0 = wm * WM, tc0 = wn * WN;
-  if (tr0 >= tm) return;
-  double c[WM][WN][2];
+// tm, tn: number of 8-row / 8-column tiles; ksteps: K / 4 (padding is zero).  Lane (g, t) ends
+// up with outputs (row 8 i + g, columns 8 j + 2 t, + 1) of tile (i, j) in c[i][j][0..1].
+template <int WM, int WN, bool AT, bool BT>
+__device__ __forceinline__ void slab_gemm(const WarpTile<WM, WN>& w, const double* __restrict__ As,
+                                          const double* __restrict__ Bs, int ld, int tm, int tn, int ksteps,
+                                          double (&c)[WM][WN][2]) {
 #pragma unroll
   for (int i = 0; i < WM; ++i)
 #pragma unroll
     for (int j = 0; j < WN; ++j) c[i][j][0] = c[i][j][1] = 0.0;
+  if (!w.active) return;
   // out-of-range tiles of a partial warp tile read tile 0 (valid memory) and are discarded
   int ao[WM], bo[WN];
 #pragma unroll
   for (int i = 0; i < WM; ++i) {
-    const int r = (tr0 + i < tm ? tr0 + i : 0) * 8 + g;
-    ao[i] = AT ? (t * ld + r) : (r * ld + t);
+    const int r = (w.tr0 + i < tm ? w.tr0 + i : 0) * 8 + w.g;
+    ao[i] = AT ? (w.t * ld + r) : (r * ld + w.t);
   }
 #pragma unroll
   for (int j = 0; j < WN; ++j) {
-    const int cc = (tc0 + j < tn ? tc0 + j : 0) * 8 + g;
-    bo[j] = BT ? (cc * ld + t) : (t * ld + cc);
+    const int cc = (w.tc0 + j < tn ? w.tc0 + j : 0) * 8 + w.g;
+    bo[j] = BT ? (cc * ld + w.t) : (w.t * ld + cc);
   }
   const int astep = AT ? 4 * ld : 4, bstep = BT ? 4 : 4 * ld;
-#pragma unroll 2
+#pragma unroll 4
   for (int ks = 0; ks < ksteps; ++ks) {
     double a[WM], b[WN];
 #pragma unroll
@@ -64,28 +85,68 @@ __device__ __forceinline__ void slab_gemm(const double* __restrict__ As, const d
 #pragma unroll
       for (int j = 0; j < WN; ++j) dmma884(c[i][j][0], c[i][j][1], a[i], b[j]);
   }
+}
+
+// every owned output pair: f(i, j, row, col) with col even
+template <int WM, int WN, class F>
+__device__ __forceinline__ void for_tiles(const WarpTile<WM, WN>& w, int tm, int tn, F f) {
+  if (!w.active) return;
 #pragma unroll
   for (int i = 0; i < WM; ++i) {
-    if (tr0 + i >= tm) break;
+    if (w.tr0 + i >= tm) break;
 #pragma unroll
     for (int j = 0; j < WN; ++j) {
-      if (tc0 + j >= tn) break;
-      epi((tr0 + i) * 8 + g, (tc0 + j) * 8 + 2 * t, c[i][j][0], c[i][j][1]);
+      if (w.tc0 + j >= tn) break;
+      f(i, j, (w.tr0 + i) * 8 + w.g, (w.tc0 + j) * 8 + 2 * w.t);
     }
   }
 }
 
-// zero-padded copy of an (nr x nc) matrix (element (r, c) at src(r, c)) into an n8r x ld buffer
-template <class Src>
-__device__ __forceinline__ void slab_fill(double* dst, int ld, int rows8, int nr, int nc, Src src) {
+// zero-padded asynchronous copy of an (nr x nc) matrix with row stride rs into a rows8 x ld
+// buffer; all copies of the CTA are in flight together (cp.async), padding is stored directly
+__device__ __forceinline__ void slab_fill(double* dst, int ld, int rows8, int nr, int nc, const double* src,
+                                          long long rs) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int r = warp; r < rows8; r += nw)
-    for (int c0 = lane; c0 < ld; c0 += 32) dst[r * ld + c0] = (r < nr && c0 < nc) ? src(r, c0) : 0.0;
+    for (int c0 = lane; c0 < ld; c0 += 32) {
+      if (r < nr && c0 < nc) cp_async8(&dst[r * ld + c0], src + r * rs + c0);
+      else dst[r * ld + c0] = 0.0;
+    }
+}
+// the same through an index list: element (r, c) = src[idx[r * nc + c]]; index loads batched
+// four rows deep so their latency is paid once per batch, not once per row
+__device__ __forceinline__ void slab_fill_gather(double* dst, int ld, int rows8, int nr, int nc,
+                                                 const double* __restrict__ src, const int* __restrict__ idx) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  constexpr int RB = 4, CB = 3;   // ld <= 96
+  for (int r0 = warp; r0 < rows8; r0 += RB * nw) {
+    int id[RB][CB];
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int r = r0 + a * nw, c0 = lane + 32 * b;
+        id[a][b] = (r < nr && c0 < nc) ? __ldg(&idx[(long long)r * nc + c0]) : -1;
+      }
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+      for (int b = 0; b < CB; ++b) {
+        const int r = r0 + a * nw, c0 = lane + 32 * b;
+        if (r < rows8 && c0 < ld) {
+          if (id[a][b] >= 0) cp_async8(&dst[r * ld + c0], src + id[a][b]);
+          else dst[r * ld + c0] = 0.0;
+        }
+      }
+  }
 }
 
+// lr_shared: T1 and T2 are the same matrix for every interior (equal spaces along the slab's two
+// axes), so one copy serves as left and right factor and stage 1 reads D from global memory: two
+// buffers instead of three, two CTAs per SM at n8 = 72.
 template <int WM, int WN, int STAGE>
-__global__ void __launch_bounds__(FD3_MAXWARPS * 32)
-fd3_kernel(const Fd3Item* __restrict__ items, int nitems, int n8, const double* __restrict__ src,
+__global__ void __launch_bounds__(FD3_MAXWARPS * 32, 2)
+fd3_kernel(const Fd3Item* __restrict__ items, int nitems, int n8, int lr_shared, const double* __restrict__ src,
            double* dst, double alpha, int accumulate) {
   pdl_begin();
   extern __shared__ __align__(16) double fd3_smem[];
@@ -104,79 +165,121 @@ fd3_kernel(const Fd3Item* __restrict__ items, int nitems, int n8, const double* 
   const int s = blockIdx.x - (STAGE == 1 ? I.slab1 : I.slab0);
   const int n0 = I.n[0], n1 = I.n[1], n2 = I.n[2];
   const int ld = n8 + 4;
-  double* S = fd3_smem;            // the slab, then the second product's left operand source
-  double* X = S + n8 * ld;         // first product
-  double* L = X + n8 * ld;         // left factor
-  double* R = L + n8 * ld;         // right factor (stage 1: the slab of D)
+  double* S = fd3_smem;            // the slab; overwritten by the first product
+  double* L = S + n8 * ld;         // left factor
+  double* R = lr_shared ? L : L + n8 * ld;   // right factor (stage 1, three buffers: the slab of D)
   const long long n12 = (long long)n1 * n2;
+  double c[WM][WN][2];
   if (STAGE != 1) {
     // slab i0 = s: rows i1, columns i2
     const long long base = (long long)s * n12;
     const int tm = (n1 + 7) >> 3, tn = (n2 + 7) >> 3;
-    if (STAGE == 0)
-      slab_fill(S, ld, tm * 8, n1, n2, [&](int r, int c) { return __ldg(&src[__ldg(&I.idx[base + (long long)r * n2 + c])]); });
-    else
-      slab_fill(S, ld, tm * 8, n1, n2, [&](int r, int c) { return I.buf1[base + (long long)r * n2 + c]; });
-    slab_fill(L, ld, tm * 8, n1, n1, [&](int r, int c) { return __ldg(&I.T[1][r * n1 + c]); });
-    slab_fill(R, ld, tn * 8, n2, n2, [&](int r, int c) { return __ldg(&I.T[2][r * n2 + c]); });
+    const WarpTile<WM, WN> w(tm, tn);
+    if (STAGE == 0) slab_fill_gather(S, ld, tm * 8, n1, n2, src, I.idx + base);
+    else slab_fill(S, ld, tm * 8, n1, n2, I.buf1 + base, n2);
+    slab_fill(L, ld, tm * 8, n1, n1, I.T[1], n1);
+    if (!lr_shared) slab_fill(R, ld, tn * 8, n2, n2, I.T[2], n2);
+    cp_async_wait_all();
     __syncthreads();
     const int k1 = (n1 + 3) >> 2, k2 = (n2 + 3) >> 2;
-    auto keep = [&](int r, int c, double v0, double v1) {
-      *reinterpret_cast<double2*>(&X[r * ld + c]) = make_double2(v0, v1);
-    };
+    // first product (T1^T S or T1 S), in place: every warp holds its outputs until all have read S
+    if (STAGE == 0) slab_gemm<WM, WN, true, false>(w, L, S, ld, tm, tn, k1, c);
+    else slab_gemm<WM, WN, false, false>(w, L, S, ld, tm, tn, k1, c);
+    __syncthreads();
+    for_tiles(w, tm, tn, [&](int i, int j, int r, int cc) {
+      *reinterpret_cast<double2*>(&S[r * ld + cc]) = make_double2(c[i][j][0], c[i][j][1]);
+    });
+    __syncthreads();
     if (STAGE == 0) {
-      // X = T1^T S ; Y = X T2
-      slab_gemm<WM, WN, true, false>(L, S, ld, tm, tn, k1, keep);
-      __syncthreads();
+      // Y = S T2
+      slab_gemm<WM, WN, false, false>(w, S, R, ld, tm, tn, k2, c);
       double* out = I.buf0 + base;
-      slab_gemm<WM, WN, false, false>(X, R, ld, tm, tn, k2, [&](int r, int c, double v0, double v1) {
+      for_tiles(w, tm, tn, [&](int i, int j, int r, int cc) {
         if (r < n1) {
-          if (c < n2) out[(long long)r * n2 + c] = v0;
-          if (c + 1 < n2) out[(long long)r * n2 + c + 1] = v1;
+          if (cc < n2) out[(long long)r * n2 + cc] = c[i][j][0];
+          if (cc + 1 < n2) out[(long long)r * n2 + cc + 1] = c[i][j][1];
         }
       });
     } else {
-      // X = T1 S ; out = X T2^T -> scatter
-      slab_gemm<WM, WN, false, false>(L, S, ld, tm, tn, k1, keep);
-      __syncthreads();
+      // out = S T2^T -> u[idx] (+)= alpha out; targets and old values are fetched in batches
       const int* idx = I.idx + base;
-      slab_gemm<WM, WN, false, true>(X, R, ld, tm, tn, k2, [&](int r, int c, double v0, double v1) {
-        if (r < n1) {
-          if (c < n2) {
-            double* d = dst + __ldg(&idx[(long long)r * n2 + c]);
-            const double sv = __dmul_rn(alpha, v0);
-            *d = accumulate ? __dadd_rn(*d, sv) : sv;
-          }
-          if (c + 1 < n2) {
-            double* d = dst + __ldg(&idx[(long long)r * n2 + c + 1]);
-            const double sv = __dmul_rn(alpha, v1);
-            *d = accumulate ? __dadd_rn(*d, sv) : sv;
-          }
-        }
+      int id[WM][WN][2];
+      for_tiles(w, tm, tn, [&](int i, int j, int r, int cc) {
+        id[i][j][0] = (r < n1 && cc < n2) ? __ldg(&idx[(long long)r * n2 + cc]) : -1;
+        id[i][j][1] = (r < n1 && cc + 1 < n2) ? __ldg(&idx[(long long)r * n2 + cc + 1]) : -1;
       });
+      slab_gemm<WM, WN, false, true>(w, S, R, ld, tm, tn, k2, c);
+      // old values and stores one tile row at a time (register budget of two CTAs per SM)
+      if (w.active) {
+#pragma unroll
+        for (int i = 0; i < WM; ++i) {
+          if (w.tr0 + i >= tm) break;
+          double old[WN][2];
+#pragma unroll
+          for (int j = 0; j < WN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              old[j][h] = (accumulate && w.tc0 + j < tn && id[i][j][h] >= 0) ? dst[id[i][j][h]] : 0.0;
+#pragma unroll
+          for (int j = 0; j < WN; ++j)
+#pragma unroll
+            for (int h = 0; h < 2; ++h)
+              if (w.tc0 + j < tn && id[i][j][h] >= 0)
+                dst[id[i][j][h]] = __dadd_rn(old[j][h], __dmul_rn(alpha, c[i][j][h]));
+        }
+      }
     }
   } else {
     // slab i1 = s: rows i0 (stride n1 n2), columns i2
     const long long base = (long long)s * n2;
     const int tm = (n0 + 7) >> 3, tn = (n2 + 7) >> 3;
-    slab_fill(S, ld, tm * 8, n0, n2, [&](int r, int c) { return I.buf0[base + (long long)r * n12 + c]; });
-    slab_fill(L, ld, tm * 8, n0, n0, [&](int r, int c) { return __ldg(&I.T[0][r * n0 + c]); });
-    slab_fill(R, ld, tm * 8, n0, n2, [&](int r, int c) { return __ldg(&I.D[base + (long long)r * n12 + c]); });
+    const WarpTile<WM, WN> w(tm, tn);
+    slab_fill(S, ld, tm * 8, n0, n2, I.buf0 + base, n12);
+    slab_fill(L, ld, tm * 8, n0, n0, I.T[0], n0);
+    if (!lr_shared) slab_fill(R, ld, tm * 8, n0, n2, I.D + base, n12);
+    cp_async_wait_all();
     __syncthreads();
     const int k0 = (n0 + 3) >> 2;
-    // X = (T0^T S) ./ D   (padding stays zero: 0 / 0 is never formed)
-    slab_gemm<WM, WN, true, false>(L, S, ld, tm, tn, k0, [&](int r, int c, double v0, double v1) {
-      const double d0 = R[r * ld + c], d1 = R[r * ld + c + 1];
-      const double q0 = (r < n0 && c < n2) ? __ddiv_rn(v0, d0) : 0.0;
-      const double q1 = (r < n0 && c + 1 < n2) ? __ddiv_rn(v1, d1) : 0.0;
-      *reinterpret_cast<double2*>(&X[r * ld + c]) = make_double2(q0, q1);
-    });
+    // S = (T0^T S) ./ D   (padding stays zero: 0 / 0 is never formed)
+    slab_gemm<WM, WN, true, false>(w, L, S, ld, tm, tn, k0, c);
     __syncthreads();
+    if (w.active) {
+      const double* Dg = I.D + base;
+#pragma unroll
+      for (int i = 0; i < WM; ++i) {
+        if (w.tr0 + i >= tm) break;
+        const int r = (w.tr0 + i) * 8 + w.g;
+        double dv[WN][2];
+#pragma unroll
+        for (int j = 0; j < WN; ++j) {
+          const int cc = (w.tc0 + j) * 8 + 2 * w.t;
+          const bool in0 = w.tc0 + j < tn && r < n0 && cc < n2, in1 = w.tc0 + j < tn && r < n0 && cc + 1 < n2;
+          if (lr_shared) {  // denominators straight from global memory (L2)
+            dv[j][0] = in0 ? __ldg(&Dg[(long long)r * n12 + cc]) : 1.0;
+            dv[j][1] = in1 ? __ldg(&Dg[(long long)r * n12 + cc + 1]) : 1.0;
+          } else if (w.tc0 + j < tn) {
+            const double2 d = *reinterpret_cast<const double2*>(&R[r * ld + cc]);
+            dv[j][0] = in0 ? d.x : 1.0;
+            dv[j][1] = in1 ? d.y : 1.0;
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < WN; ++j) {
+          if (w.tc0 + j >= tn) break;
+          const int cc = (w.tc0 + j) * 8 + 2 * w.t;
+          const double q0 = (r < n0 && cc < n2) ? __ddiv_rn(c[i][j][0], dv[j][0]) : 0.0;
+          const double q1 = (r < n0 && cc + 1 < n2) ? __ddiv_rn(c[i][j][1], dv[j][1]) : 0.0;
+          *reinterpret_cast<double2*>(&S[r * ld + cc]) = make_double2(q0, q1);
+        }
+      }
+    }
+    __syncthreads();
+    slab_gemm<WM, WN, false, false>(w, L, S, ld, tm, tn, k0, c);
     double* out = I.buf1 + base;
-    slab_gemm<WM, WN, false, false>(L, X, ld, tm, tn, k0, [&](int r, int c, double v0, double v1) {
+    for_tiles(w, tm, tn, [&](int i, int j, int r, int cc) {
       if (r < n0) {
-        if (c < n2) out[(long long)r * n12 + c] = v0;
-        if (c + 1 < n2) out[(long long)r * n12 + c + 1] = v1;
+        if (cc < n2) out[(long long)r * n12 + cc] = c[i][j][0];
+        if (cc + 1 < n2) out[(long long)r * n12 + cc + 1] = c[i][j][1];
       }
     });
   }
@@ -186,24 +289,24 @@ template <int WM, int WN>
 void launch_fd3_t(cudaStream_t s, const Fd3Plan& P, int stage, const double* r, double* u, double alpha,
                   int accumulate) {
   static bool attr = false;
-  const size_t smem_max = 4ull * FD3_NMAX * (FD3_NMAX + 4) * sizeof(double);
+  const size_t smem_max = 3ull * FD3_NMAX * (FD3_NMAX + 4) * sizeof(double);
   if (!attr) {
     cudaFuncSetAttribute(fd3_kernel<WM, WN, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     cudaFuncSetAttribute(fd3_kernel<WM, WN, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     cudaFuncSetAttribute(fd3_kernel<WM, WN, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_max);
     attr = true;
   }
-  const size_t smem = 4ull * P.n8 * (P.n8 + 4) * sizeof(double);
+  const size_t smem = (P.lr_shared ? 2ull : 3ull) * P.n8 * (P.n8 + 4) * sizeof(double);
   const int t8 = P.n8 / 8;
   const int warps = ((t8 + WM - 1) / WM) * ((t8 + WN - 1) / WN);
   if (stage == 0)
-    launch_k(fd3_kernel<WM, WN, 0>, dim3(P.slabs0), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, r,
+    launch_k(fd3_kernel<WM, WN, 0>, dim3(P.slabs0), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, P.lr_shared, r,
              (double*)nullptr, alpha, accumulate);
   else if (stage == 1)
-    launch_k(fd3_kernel<WM, WN, 1>, dim3(P.slabs1), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, r,
+    launch_k(fd3_kernel<WM, WN, 1>, dim3(P.slabs1), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, P.lr_shared, r,
              (double*)nullptr, alpha, accumulate);
   else
-    launch_k(fd3_kernel<WM, WN, 2>, dim3(P.slabs0), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, r, u,
+    launch_k(fd3_kernel<WM, WN, 2>, dim3(P.slabs0), dim3(32 * warps), smem, s, P.d_items, P.nitems, P.n8, P.lr_shared, r, u,
              alpha, accumulate);
 }
 

@@ -1029,6 +1029,9 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
       }
       P.nitems = (int)items.size();
       P.n8 = (nmax + 7) / 8 * 8;
+      P.lr_shared = 1;
+      for (auto& I : items) P.lr_shared &= (I.T[1] == I.T[2] && I.n[1] == I.n[2]) ? 1 : 0;
+      if (std::getenv("IGB_FD3_BUF3")) P.lr_shared = 0;
       P.d_items = ctx->upload(items.data(), items.size());
       return;
     }

@@ -276,6 +276,7 @@ struct Fd3Item {
 struct Fd3Plan {
   Fd3Item* d_items = nullptr;
   int nitems = 0, n8 = 0, slabs0 = 0, slabs1 = 0;
+  int lr_shared = 0;    // every interior has T[1] == T[2]: two shared-memory buffers per CTA
 };
 void launch_fd3(cudaStream_t s, const Fd3Plan& P, int stage, const double* r, double* u, double alpha, int accumulate);
 void fd3_set_carveout(int pct);

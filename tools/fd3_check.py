@@ -18,6 +18,7 @@ ap.add_argument("--levels", type=int, default=None)
 ap.add_argument("--p", type=int, default=None)
 ap.add_argument("--solves", type=int, default=3)
 ap.add_argument("--no-oracle", action="store_true")
+ap.add_argument("--ops", type=int, default=0, help="plain (non-graph) SCMS applications on the finest level, for ncu")
 args = ap.parse_args()
 
 from paper_1902_01818_b200 import configs, multigrid  # noqa: E402
@@ -42,6 +43,13 @@ if not args.no_oracle:
         a = ctx.op("scms", level, x, n)
         b = orc.scms_apply(level, x)
         print(f"level {level} n {n}: scms rel diff {np.linalg.norm(a - b) / np.linalg.norm(b):.2e}", flush=True)
+if args.ops:
+    xr = np.random.default_rng(5).standard_normal(len(f))
+    for _ in range(args.ops):
+        ctx.op("scms", solver.finest, xr, len(f))
+    print("ops done", flush=True)
+    solver.close()
+    sys.exit(0)
 d_b = ctx.device_alloc(8 * len(f))
 d_x = ctx.device_alloc(8 * len(f))
 ctx.h2d(d_b, f)

@@ -63,7 +63,7 @@ SIGNATURES = {
 PREC = {"none": 0, "cycle": 1, "host": 2}
 PREC_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(_d), ctypes.POINTER(_d), _i, _p)
 ITER_FN = ctypes.CFUNCTYPE(None, _i, _d, _p)
-GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule", 5: "line"}
+GS_ENGINES = {1: "panel", 2: "flow", 3: "levelset", 4: "schedule", 5: "line", 6: "wave"}
 
 _lib = None
 

@@ -9,7 +9,7 @@ NVCC="${NVCC:-nvcc}"
 "$NVCC" -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -lineinfo \
   -Xcompiler -fPIC -Xcompiler -Wall -Xlinker --no-undefined -shared -I"$ROOT/include" -I"$HERE" \
   ${IGB_NVCC_EXTRA:-} \
-  -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/panel.cu" "$HERE/fd.cu" "$HERE/fd3.cu" "$HERE/flow.cu" "$HERE/line.cu" "$HERE/transfer.cu" "$HERE/mfree.cu" "$HERE/igb.cu" "$HERE/level_plan.cpp" "$HERE/panel_plan.cpp" "$HERE/flow_plan.cpp" "$HERE/line_plan.cpp" -Xcompiler -pthread
+  -o "$OUT.tmp" "$HERE/kernels.cu" "$HERE/panel.cu" "$HERE/fd.cu" "$HERE/fd3.cu" "$HERE/flow.cu" "$HERE/line.cu" "$HERE/wave.cu" "$HERE/transfer.cu" "$HERE/mfree.cu" "$HERE/igb.cu" "$HERE/level_plan.cpp" "$HERE/panel_plan.cpp" "$HERE/flow_plan.cpp" "$HERE/line_plan.cpp" "$HERE/wave_plan.cpp" -Xcompiler -pthread
 mv "$OUT.tmp" "$OUT"
 echo "built $OUT"
 # host setup library (OpenMP, no CUDA): bit-identical native replacements of the SciPy setup steps

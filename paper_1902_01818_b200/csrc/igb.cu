@@ -27,6 +27,7 @@
 #include "level_plan.h"
 #include "flow_plan.h"
 #include "line_plan.h"
+#include "wave_plan.h"
 #include "panel_plan.h"
 #include "host_par.h"
 #include "kernels.cuh"
@@ -122,6 +123,14 @@ struct LineDev {
   int nl = 0, max_line = 0;
 };
 
+struct WaveDev {
+  bool ok = false;
+  WaveArgs args{};
+  int nlev = 0, nframes = 0, occupancy = 0;
+  long long internal = 0, external = 0;
+  double stream_bytes = 0;
+};
+
 struct Level {
   int n = 0;
   DevCsr A;
@@ -131,6 +140,7 @@ struct Level {
   PanelDev panel[2];   // row-panel sweeps (preferred when built)
   FlowDev flow[2];     // dependency-driven whole-GPU sweeps (wide levels, long rows)
   LineDev line[2];     // line sweeps (bundles of grid lines per CTA; 3-D levels)
+  WaveDev wave[2];     // wave sweeps (plane chains inside one CTA, external sums GPU-wide)
   double* xg = nullptr;  // panel sweep solution by position (old values)
   double* rp = nullptr;   // level-ordered right-hand side / solution of the sweep
   double* xp = nullptr;
@@ -422,6 +432,45 @@ struct igb_ctx {
                      l, upper ? 1 : 0, V.n, hd[0], hd[1] / np, hd[2] / np, hd[3] / np, hd[4] / np, hd[5] / np,
                      hd[6] / np, hd[7] / np);
       }
+      return;
+    }
+    WaveDev& Wv = V.wave[upper ? 1 : 0];
+    if (Wv.ok) {
+      WaveArgs a = Wv.args;
+      a.res = rhs;
+      a.u = u;
+      a.accumulate = u_zero ? 0 : 1;
+      const long long tri = upper ? V.tri_nnz_upper : V.tri_nnz_lower;
+      const double bytes = 12.0 * (tri + V.n) + 4.0 * (V.n + 1) + 24.0 * V.n;
+      static const bool want_dbg = std::getenv("IGB_GS_DEBUG") != nullptr;
+      if (want_dbg && !capturing) {
+        cudaEvent_t e0, e1;
+        CU(cudaEventCreate(&e0));
+        CU(cudaEventCreate(&e1));
+        static unsigned long long* wdbg = nullptr;
+        if (!wdbg) CU(cudaMalloc(&wdbg, 16 * sizeof(unsigned long long)));
+        CU(cudaMemsetAsync(wdbg, 0, 16 * sizeof(unsigned long long), stream));
+        a.dbg = wdbg;
+        CU(cudaEventRecord(e0, stream));
+        launch_wave_sweep(stream, a);
+        CU(cudaEventRecord(e1, stream));
+        CU(cudaEventSynchronize(e1));
+        float ms = 0;
+        CU(cudaEventElapsedTime(&ms, e0, e1));
+        unsigned long long hd[16];
+        CU(cudaMemcpy(hd, wdbg, sizeof(hd), cudaMemcpyDeviceToHost));
+        const double fr = (double)std::max(1ULL, hd[0]), pr = (double)std::max(1ULL, hd[6]);
+        std::fprintf(stderr, "[gs dbg] wave level %d dir %d n %d depth %d bundles %d ctas %d: %.1f us, %.3f us/level, "
+                     "%.0f GB/s streamed; compute %.0f cyc/frame (%.0f waiting for the queue), poller quad 0: "
+                     "%.0f cyc/row late wait, %.0f ext wait, %.0f queue-space wait\n", l, upper ? 1 : 0, V.n, Wv.nlev,
+                     a.nb, a.ctas, ms * 1e3, ms * 1e3 / std::max(1, Wv.nlev), Wv.stream_bytes / (ms * 1e6), hd[1] / fr,
+                     hd[2] / fr, hd[4] / pr, hd[5] / pr, hd[7] / pr);
+
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        return;
+      }
+      launch(K_GS, bytes, [&] { launch_wave_sweep(stream, a); });
       return;
     }
     LineDev& Ln = V.line[upper ? 1 : 0];
@@ -1577,6 +1626,81 @@ double flow_min_width() {
   return w;
 }
 
+// Wave sweep for one direction (wave_plan.h, wave.cu).
+bool build_wave_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
+  const char* mn = std::getenv("IGB_WAVE_RBMIN");
+  const char* mx = std::getenv("IGB_WAVE_RBMAX");
+  const char* le = std::getenv("IGB_WAVE_CRITLAG");
+  const char* lm = std::getenv("IGB_WAVE_LATE");
+  const char* ll = std::getenv("IGB_WAVE_LATELAG");
+  const int late_lag = ll ? std::max(0, std::atoi(ll)) : 9;
+  const int rb_min = mn ? std::max(1, std::atoi(mn)) : 32;
+  const int rb_cap = mx ? std::max(64, std::atoi(mx)) : 8192;
+  const int lag = le ? std::max(1, std::atoi(le)) : 4;
+  const int late_max = lm ? std::max(0, std::atoi(lm)) : 32;
+  int cap = wave_max_ctas(wave_smem_bytes(rb_cap));
+  if (const char* ce = std::getenv("IGB_WAVE_CTAS")) cap = std::min(cap, std::max(1, std::atoi(ce)));
+  if (cap < 1) return false;
+  WavePlanHost plan;
+  if (!build_wave_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1, rb_min, rb_cap,
+                       late_lag, lag, late_max, cap, plan)) {
+    if (std::getenv("IGB_VERBOSE"))
+      std::fprintf(stderr, "[igb] level %d dir %d: no wave plan (bundles %d, occupancy %d of %d CTAs)\n", level, dir,
+                   plan.nb, plan.occupancy, cap);
+    return false;
+  }
+  WaveDev& D = V.wave[dir];
+  WaveArgs& a = D.args;
+  a = WaveArgs{};
+  a.n = V.n;
+  a.nb = plan.nb;
+  a.nq = plan.nq;
+  a.rb_max = plan.rb_max;
+  a.xs_len = wave_xs_len(plan.rb_max);
+  a.ctas = std::min(cap, std::max(1, wave_max_ctas(wave_smem_bytes(plan.rb_max))));
+  a.b_frame = ctx->upload(plan.b_frame.data(), plan.b_frame.size());
+  a.b_start = ctx->upload(plan.b_start.data(), plan.b_start.size());
+  a.f_end = ctx->upload(plan.f_end.data(), plan.f_end.size());
+  a.hdr = ctx->upload(plan.hdr.data(), plan.hdr.size());
+  a.lcol = ctx->upload(plan.lcol.data(), plan.lcol.size());
+  a.lval = ctx->upload(plan.lval.data(), plan.lval.size());
+  a.recA = ctx->upload(plan.recA.data(), plan.recA.size());
+  a.recB = ctx->upload(plan.recB.data(), plan.recB.size());
+  a.e_row = plan.nq ? ctx->upload(plan.e_row.data(), plan.e_row.size()) : ctx->alloc<int>(1);
+  a.eptr = ctx->upload(plan.eptr.data(), plan.eptr.size());
+  a.ecol = plan.external ? ctx->upload(plan.ecol.data(), plan.ecol.size()) : ctx->alloc<int>(1);
+  a.eval = plan.external ? ctx->upload(plan.eval.data(), plan.eval.size()) : ctx->alloc<double>(1);
+  a.crit = plan.nq ? ctx->upload(plan.crit.data(), plan.crit.size()) : ctx->alloc<int>(1);
+  a.elate = plan.nq ? ctx->upload(plan.elate.data(), plan.elate.size()) : ctx->alloc<int>(1);
+  const char* be = std::getenv("IGB_WAVE_BACKOFF");
+  a.backoff = be ? std::atoi(be) : 128;
+  const char* pbe = std::getenv("IGB_WAVE_PBACKOFF");
+  a.pbackoff = pbe ? std::atoi(pbe) : 32;
+  std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF2468ULL);  // wave.cu WAVE_PENDING
+  a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
+  a.eg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
+  int* ctr = ctx->alloc<int>(4);
+  CU(cudaMemset(ctr, 0, 4 * sizeof(int)));
+  a.par_ctr = ctr;
+  a.done_ctr = reinterpret_cast<unsigned*>(ctr + 1);
+  a.ticket = ctr + 2;
+  D.nlev = plan.nlev;
+  D.nframes = plan.nframes;
+  D.occupancy = plan.occupancy;
+  D.internal = plan.internal;
+  D.external = plan.external;
+  // external entries, lane records (32 B each), slot headers, external-list metadata, vectors
+  D.stream_bytes = 12.0 * plan.external + 32.0 * plan.recA.size() + (16.0 + 12.0 * WAVE_LN) * V.n + 20.0 * plan.nq +
+                   56.0 * V.n;
+  D.ok = true;
+  if (std::getenv("IGB_VERBOSE"))
+    std::fprintf(stderr, "[igb] level %d dir %d: wave sweep n %d depth %d bundles %d (max rows %d, widest level %d) frames %d "
+                 "internal %lld demoted %lld late %lld external %lld (%d rows) occupancy %d ctas %d stream %.1f MB\n", level, dir,
+                 V.n, plan.nlev, plan.nb, plan.rb_max, plan.max_level_rows, plan.nframes, plan.internal, plan.demoted,
+                 plan.late, plan.external, plan.nq, plan.occupancy, a.ctas, D.stream_bytes / 1e6);
+  return true;
+}
+
 // Line sweep for one direction (line_plan.h, line.cu).
 bool build_line_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vector<int>& dp) {
   const char* mn = std::getenv("IGB_LINE_RBMIN");
@@ -1741,6 +1865,12 @@ int igb_set_gs(igb_ctx* ctx, int level) {
       }
     }
     lap("panel plans");
+    // wave sweep (plane chains inside one CTA): IGB_GS_ENGINE=wave forces it on every level
+    if (engine == "wave") {
+      for (int dir = 0; dir < 2; ++dir)
+        if (!panel_done[dir]) panel_done[dir] = build_wave_sweep(ctx, V, level, dir, dp);
+      lap("wave plans");
+    }
     // line sweep (bundles of grid lines per CTA): IGB_GS_ENGINE=line forces it on every level
     if (engine == "line") {
       for (int dir = 0; dir < 2; ++dir)
@@ -2629,6 +2759,9 @@ int igb_gs_info(igb_ctx* ctx, int level, int dir, int* info, int ninfo) {
     if (V.panel[dir].ok) {
       const PanelArgs& a = V.panel[dir].args;
       v[0] = 1; v[1] = a.B; v[2] = a.KA; v[3] = a.KF; v[4] = a.nclu; v[5] = a.npan;
+    } else if (V.wave[dir].ok) {
+      v[0] = 6; v[1] = V.wave[dir].args.rb_max; v[4] = V.wave[dir].args.nb; v[5] = V.wave[dir].nframes;
+      v[6] = V.wave[dir].nlev;
     } else if (V.line[dir].ok) {
       v[0] = 5; v[1] = V.line[dir].args.rb_max; v[2] = V.line[dir].args.C; v[4] = V.line[dir].args.nb;
       v[5] = V.line[dir].nl;

@@ -806,6 +806,7 @@ void carveout_prepare() {
   kron_set_carveout(pct);
   mf_set_carveout(pct);
   fd3_set_carveout(pct);
+  wave_set_carveout(pct);
 }
 
 size_t level_smem_bytes(const LevelArgs& a) { return 8 * (size_t)a.R; }

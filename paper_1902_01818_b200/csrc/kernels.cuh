@@ -164,6 +164,43 @@ int flow_max_ctas();  // co-resident CTAs of FLOW_NT threads (all variants)
 void flow_set_carveout(int pct);
 void launch_flow_sweep(cudaStream_t s, const FlowArgs& a);
 
+// ---- wave sweep: GS with the dependency chain inside one CTA per grid plane (wave.cu, wave_plan.h)
+constexpr int WAVE_NT = 1024;  // 32 warps per CTA, one CTA per SM
+struct WaveHdr;
+struct WaveRecA;
+struct WaveRecB;
+struct WaveArgs {
+  const int* b_frame;  // [nb + 1] first frame of each bundle
+  const int* b_start;  // [nb + 1] first row (sweep order) of each bundle
+  const int* f_end;    // [nframes] rows of the frame's bundle in frames up to and including it
+  const WaveHdr* hdr;  // [n] sweep order
+  const int* lcol;     // [n * LN] late entries (rows, -1 none)
+  const double* lval;
+  const WaveRecA* recA;
+  const WaveRecB* recB;
+  const int* e_row;    // external list (flow layout)
+  const int* eptr;
+  const int* ecol;
+  const double* eval;
+  const int* crit;
+  const int* elate;
+  const double* res;   // right-hand side by row
+  double* u;           // u (+)= c by row
+  double* xg;          // [2][n] solution by row, pending until produced
+  double* eg;          // [2][n] external sums by row, pending until produced
+  int* par_ctr;        // sweep parity of this level and direction (device)
+  unsigned* done_ctr;  // CTAs finished (device), reset by the last one
+  int* ticket;         // next bundle to hand out (device), rewound by the last CTA
+  int n, nb, nq, ctas, accumulate, backoff, pbackoff;   // backoff: ns slept between polls (external warps / pollers)
+  int rb_max, xs_len;
+  unsigned long long* dbg;   // nullable: 8 counters (wave.cu)
+};
+size_t wave_smem_bytes(int rb_max);
+int wave_xs_len(int rb_max);
+int wave_max_ctas(size_t smem);
+void wave_set_carveout(int pct);
+void launch_wave_sweep(cudaStream_t s, const WaveArgs& a);
+
 // ---- line sweep: GS along grid lines, bundles of lines per CTA (line.cu, line_plan.h) -------
 constexpr int LINE_NT = 512;  // 16 warps per CTA
 struct LineArgs {

@@ -1,0 +1,4 @@
+export PYTHONUNBUFFERED=1 IGB_VERBOSE=1 IGB_GS_DEBUG=1 IGB_GS_ENGINE=wave
+timeout 300 python tools/engine_check.py cfg5:levels=1 > gpurun_out/r2_wave_L1.log 2>&1; echo "rc=$?" >> gpurun_out/r2_wave_L1.log
+timeout 400 python tools/engine_check.py cfg5:levels=2 > gpurun_out/r2_wave_L2.log 2>&1; echo "rc=$?" >> gpurun_out/r2_wave_L2.log
+timeout 600 python tools/engine_check.py cfg5:levels=3 > gpurun_out/r2_wave_L3.log 2>&1; echo "rc=$?" >> gpurun_out/r2_wave_L3.log

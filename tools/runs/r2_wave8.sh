@@ -1,0 +1,2 @@
+export PYTHONUNBUFFERED=1 IGB_VERBOSE=1 IGB_GS_DEBUG=1 IGB_GS_ENGINE=wave IGB_WAVE_TRACE=gpurun_out/wtrace
+timeout 600 python tools/engine_check.py cfg5:levels=2:nooracle > gpurun_out/r2_wave_L2t.log 2>&1; echo "rc=$?" >> gpurun_out/r2_wave_L2t.log

@@ -2341,18 +2341,21 @@ static void build_pcg_graph(igb_ctx* ctx, const double* d_b, double* d_x, int ma
     CU(cudaStreamBeginCaptureToGraph(ctx->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     c0 = ctx->graph_kernels;
     ctx->cg_matvec(s);
+    // x / r update, residual norm and history, and (last block) the loop conditions: one launch
     ctx->launch(K_CG, 56.0 * n, [&] {
-      launch_cg_update(s, n, d_x, r, ctx->d, ctx->q, ctx->partials, ctx->counter, ctx->sc, ctx->hist_dev);
+      launch_cg_update_cond(s, n, d_x, r, ctx->d, ctx->q, ctx->partials, ctx->counter, ctx->sc, ctx->hist_dev, loop, more,
+                            max_iters);
     });
-    ctx->launch(K_CG, 0.0, [&] { launch_cg_cond(s, loop, more, ctx->sc, max_iters, 0); });
     ctx->pcg_n_head = ctx->graph_kernels - c0;
     cudaGraph_t ifbody = add_cond(ctx->stream, more, cudaGraphCondTypeIf);
     ctx->stream = ctx->aux[1];
     CU(cudaStreamBeginCaptureToGraph(ctx->stream, ifbody, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
     c0 = ctx->graph_kernels;
     ctx->cycle(L, r, z);
-    ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, r, z, ctx->partials, ctx->counter, ctx->sc, FIN_BETA, nullptr); });
-    ctx->launch(K_CG, 24.0 * n, [&] { launch_cg_direction(s, n, ctx->d, z, ctx->sc); });
+    // beta = (r.z) / rz_old and d = z + beta d: one persistent launch
+    ctx->launch(K_CG, 32.0 * n, [&] {
+      launch_cg_beta_direction(s, n, ctx->d, z, r, ctx->partials, ctx->counter, ctx->sc);
+    });
     ctx->pcg_n_if = ctx->graph_kernels - c0;
     CU(cudaStreamEndCapture(ctx->aux[1], &ifbody));
     CU(cudaStreamEndCapture(ctx->aux[0], &body));
@@ -2481,10 +2484,9 @@ static bool pcg_core(igb_ctx* ctx, const double* d_b, double tol, int max_iters,
     if (it == max_iters) break;
     ctx->run_finest_cycle();
     ++ncycles;
-    ctx->launch(K_CG, 16.0 * n, [&] {
-      launch_dot(s, n, r, z, ctx->partials, ctx->counter, ctx->sc, FIN_BETA, nullptr);
+    ctx->launch(K_CG, 32.0 * n, [&] {
+      launch_cg_beta_direction(s, n, ctx->d, z, r, ctx->partials, ctx->counter, ctx->sc);
     });
-    ctx->launch(K_CG, 24.0 * n, [&] { launch_cg_direction(s, n, ctx->d, z, ctx->sc); });
   }
   CU(cudaEventRecord(ctx->t1, s));
   CU(cudaEventSynchronize(ctx->t1));
@@ -2655,8 +2657,16 @@ int igb_cg(igb_ctx* ctx, int n, long long nnz, const int* indptr, const int* ind
       ctx->launch(K_CG, 16.0 * n, [&] { launch_copy(s, n, dd, dz); });
       ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dr, dz, partials, counter, sc, FIN_RZ0, nullptr); });
       for (int it = 1; it <= max_iters; ++it) {
-        matvec();
-        ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dd, dq, partials, counter, sc, FIN_ALPHA, nullptr); });
+        if (finest_op && !ctx->lev[ctx->L].has_mf) {
+          // the same fused product + d.q as the device PCG (cg_matvec): identical bits on both paths
+          const DevCsr& A = ctx->lev[ctx->L].A;
+          ctx->launch(K_SPMV, 12.0 * A.nnz + 4.0 * (n + 1) + 24.0 * n, [&] {
+            launch_spmv_dot(s, n, A.ptr, A.col, A.val, dd, dq, A.group, partials, counter, sc, nullptr);
+          });
+        } else {
+          matvec();
+          ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dd, dq, partials, counter, sc, FIN_ALPHA, nullptr); });
+        }
         ctx->launch(K_CG, 56.0 * n, [&] { launch_cg_update(s, n, dx, dr, dd, dq, partials, counter, sc, dh); });
         CU(cudaMemcpyAsync(&h, sc, sizeof(h), cudaMemcpyDeviceToHost, s));
         CU(cudaStreamSynchronize(s));
@@ -2664,8 +2674,7 @@ int igb_cg(igb_ctx* ctx, int n, long long nnz, const int* indptr, const int* ind
         if (iter_cb) iter_cb(it, h.rel, iter_user);
         if (h.done || it == max_iters) break;
         apply_prec();
-        ctx->launch(K_CG, 16.0 * n, [&] { launch_dot(s, n, dr, dz, partials, counter, sc, FIN_BETA, nullptr); });
-        ctx->launch(K_CG, 24.0 * n, [&] { launch_cg_direction(s, n, dd, dz, sc); });
+        ctx->launch(K_CG, 32.0 * n, [&] { launch_cg_beta_direction(s, n, dd, dz, dr, partials, counter, sc); });
       }
     }
     CU(cudaMemcpyAsync(x, dx, 8 * (size_t)n, cudaMemcpyDeviceToHost, s));

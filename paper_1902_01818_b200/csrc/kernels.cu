@@ -57,13 +57,19 @@ __device__ void apply_finalize(CgScalars* sc, int kind, double sum, double* hist
       if (rel <= sc->tol) sc->done = 1;
       break;
     }
-    case FIN_BETA: sc->beta = sum / sc->rz; sc->rz = sum; break;
+    case FIN_BETA:
+      sc->beta = sum / sc->rz;
+      sc->rz = sum;
+      __threadfence();
+      *(volatile int*)&sc->beta_epoch = sc->it;
+      break;
   }
 }
 
 // Publish the block partial; the last block to arrive reduces all partials in
 // index order (deterministic for a fixed grid) and applies the finalize step.
-__device__ void finish_reduction(double blocksum, double* partials, unsigned* counter,
+// Returns true in thread 0 of that last block, after the finalize step.
+__device__ bool finish_reduction(double blocksum, double* partials, unsigned* counter,
                                  CgScalars* sc, int kind, double* hist) {
   __shared__ bool last;
   __shared__ double red2[32];
@@ -74,7 +80,7 @@ __device__ void finish_reduction(double blocksum, double* partials, unsigned* co
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (!last) return;
+  if (!last) return false;
   __threadfence();
   double v = 0.0;
 #pragma unroll 8
@@ -83,7 +89,9 @@ __device__ void finish_reduction(double blocksum, double* partials, unsigned* co
   if (threadIdx.x == 0) {
     apply_finalize(sc, kind, v, hist);
     *counter = 0u;
+    return true;
   }
+  return false;
 }
 
 // ---------------------------------------------------------------------------
@@ -660,12 +668,18 @@ __global__ void __launch_bounds__(256) dot_kernel(int n, const double* __restric
   finish_reduction(bs, partials, counter, sc, kind, hist);
 }
 
+// COND: the last block also sets the conditions of the captured PCG loop (continue the WHILE
+// node, run the IF node with the preconditioner and direction update) -- one launch less per
+// iteration than a separate condition kernel.
+template <bool COND>
 __global__ void __launch_bounds__(256) cg_update_kernel(int n, double* __restrict__ x,
                                                         double* __restrict__ r,
                                                         const double* __restrict__ d,
                                                         const double* __restrict__ q,
                                                         double* partials, unsigned* counter,
-                                                        CgScalars* sc, double* hist) {
+                                                        CgScalars* sc, double* hist,
+                                                        cudaGraphConditionalHandle loop,
+                                                        cudaGraphConditionalHandle more, int max_iters) {
   pdl_begin();
   __shared__ double red[32];
   if (sc->done) return;
@@ -678,7 +692,44 @@ __global__ void __launch_bounds__(256) cg_update_kernel(int n, double* __restric
     acc = fma(ri, ri, acc);
   }
   const double bs = block_sum(acc, red);
-  finish_reduction(bs, partials, counter, sc, FIN_REL, hist);
+  const bool fin = finish_reduction(bs, partials, counter, sc, FIN_REL, hist);
+  if (COND && fin) {
+    const unsigned cont = !sc->done && sc->it < max_iters;
+    cudaGraphSetConditional(loop, cont);
+    cudaGraphSetConditional(more, cont);
+  }
+}
+
+// beta = (r.z) / rz_old and d = z + beta d in one launch (linsolve.py:97-100).  The grid is
+// persistent and co-resident (launch_cg_beta_direction caps it at the occupancy limit): every
+// block publishes its partial of r.z, the last one to arrive reduces them in index order, stores
+// beta and the iteration number it belongs to; the others wait for that number and then update
+// their share of d.  z is read twice, the second time from L2.
+__global__ void __launch_bounds__(256) cg_beta_direction_kernel(int n, double* __restrict__ d,
+                                                                const double* __restrict__ z,
+                                                                const double* __restrict__ r, double* partials,
+                                                                unsigned* counter, CgScalars* sc) {
+  pdl_begin();
+  __shared__ double red[32];
+  __shared__ double s_beta;
+  if (sc->done) return;
+  const int epoch = sc->it;  // changes only in cg_update
+  double acc = 0.0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    acc = fma(r[i], z[i], acc);
+  const double bs = block_sum(acc, red);
+  finish_reduction(bs, partials, counter, sc, FIN_BETA, nullptr);
+  if (threadIdx.x == 0) {
+    const long long w0 = clock64();
+    while (*(volatile int*)&sc->beta_epoch != epoch)
+      if (clock64() - w0 > (1LL << 31)) __trap();
+    __threadfence();
+    s_beta = *(volatile double*)&sc->beta;
+  }
+  __syncthreads();
+  const double beta = s_beta;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    d[i] = __dadd_rn(z[i], __dmul_rn(beta, d[i]));
 }
 
 __global__ void __launch_bounds__(256) cg_direction_kernel(int n, double* __restrict__ d,
@@ -797,7 +848,8 @@ void carveout_prepare() {
       (const void*)level_sweep_kernel<false, true>, (const void*)level_sweep_kernel<true, true>,
       (const void*)perm_gather_kernel, (const void*)perm_scatter_kernel, (const void*)coarse_csc_kernel<true>,
       (const void*)coarse_csc_kernel<false>, (const void*)fd_gemm_kernel,
-      (const void*)piece_gemv_kernel, (const void*)dot_kernel, (const void*)cg_update_kernel,
+      (const void*)piece_gemv_kernel, (const void*)dot_kernel, (const void*)cg_update_kernel<false>,
+      (const void*)cg_update_kernel<true>, (const void*)cg_beta_direction_kernel,
       (const void*)cg_direction_kernel, (const void*)copy_kernel, (const void*)fill_kernel};
   for (const void* f : funcs) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pct);
   cudaGetLastError();
@@ -883,7 +935,30 @@ void launch_dot(cudaStream_t s, int n, const double* a, const double* b, double*
 void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double* d,
                       const double* q, double* partials, unsigned* counter, CgScalars* sc,
                       double* hist) {
-  launch_k(cg_update_kernel, dim3(reduction_grid(n)), dim3(256), 0, s, n, x, r, d, q, partials, counter, sc, hist);
+  launch_k(cg_update_kernel<false>, dim3(reduction_grid(n)), dim3(256), 0, s, n, x, r, d, q, partials, counter, sc, hist,
+           (cudaGraphConditionalHandle)0, (cudaGraphConditionalHandle)0, 0);
+}
+
+void launch_cg_update_cond(cudaStream_t s, int n, double* x, double* r, const double* d, const double* q,
+                           double* partials, unsigned* counter, CgScalars* sc, double* hist,
+                           cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more, int max_iters) {
+  launch_k(cg_update_kernel<true>, dim3(reduction_grid(n)), dim3(256), 0, s, n, x, r, d, q, partials, counter, sc, hist,
+           loop, more, max_iters);
+}
+
+void launch_cg_beta_direction(cudaStream_t s, int n, double* d, const double* z, const double* r, double* partials,
+                              unsigned* counter, CgScalars* sc) {
+  static int cap = 0;
+  if (!cap) {
+    int dev = 0, sms = 0, per = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, cg_beta_direction_kernel, 256, 0);
+    cudaGetLastError();
+    cap = std::max(1, per * sms);
+  }
+  launch_k(cg_beta_direction_kernel, dim3(std::min(reduction_grid(n), cap)), dim3(256), 0, s, n, d, z, r, partials,
+           counter, sc);
 }
 
 void launch_cg_cond(cudaStream_t s, cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,

@@ -368,6 +368,7 @@ struct CgScalars {
   double normb, rz, alpha, beta, rel, tol;
   int it, done;
   double pAp, rr;
+  int beta_epoch, pad;   // iteration whose beta is published (cg_beta_direction's in-kernel hand-over)
 };
 enum FinalizeKind { FIN_NORMB = 0, FIN_RZ0 = 1, FIN_ALPHA = 2, FIN_REL = 3, FIN_BETA = 4 };
 
@@ -386,6 +387,15 @@ void launch_cg_update(cudaStream_t s, int n, double* x, double* r, const double*
                       double* hist);
 // d = z + beta d
 void launch_cg_direction(cudaStream_t s, int n, double* d, const double* z, const CgScalars* sc);
+// the same two steps in one persistent launch: beta = (r.z) / rz_old by the last block to arrive,
+// every block waits for it and updates its part of d = z + beta d (linsolve.py:97-100)
+void launch_cg_beta_direction(cudaStream_t s, int n, double* d, const double* z, const double* r, double* partials,
+                              unsigned* counter, CgScalars* sc);
+// cg_update whose last block also sets the device-side loop conditions (replaces launch_cg_cond
+// after the update inside the captured PCG graph)
+void launch_cg_update_cond(cudaStream_t s, int n, double* x, double* r, const double* d, const double* q,
+                           double* partials, unsigned* counter, CgScalars* sc, double* hist,
+                           cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more, int max_iters);
 // sets the WHILE (loop) and IF (more) conditions of the device-resident PCG graph
 void launch_cg_cond(cudaStream_t s, cudaGraphConditionalHandle loop, cudaGraphConditionalHandle more,
                     const CgScalars* sc, int max_iters, int start);

@@ -17,6 +17,7 @@ import numpy as np
 import pytest
 
 from conftest import get_setup
+from test_gpu_parity import hist_ok
 
 pytestmark = pytest.mark.gpu
 
@@ -44,17 +45,19 @@ def test_cg_plain_host_callable_and_live_callback():
     from paper_1902_01818_b200 import linsolve
     pr, setup, f, solver, orc = solver_for("cfg1", levels=1)
     A = solver.A[solver.finest]
-    # plain CG
-    x, its, h = linsolve.cg(A, f, None, tol=1e-8, max_iters=2000)
-    xo, itso, ho = ocg(A, f, None, tol=1e-8, max_iters=2000)
+    # plain CG (a random right-hand side: the configuration's own f is an eigenvector of the
+    # single-patch operator, so plain CG on it stops after one step at rounding-noise level)
+    fr = np.random.default_rng(1).standard_normal(len(f))
+    x, its, h = linsolve.cg(A, fr, None, tol=1e-8, max_iters=2000)
+    xo, itso, ho = ocg(A, fr, None, tol=1e-8, max_iters=2000)
     assert its == itso
     assert np.max(np.abs(np.array(h) - ho)) / ho[0] <= 1e-10
     assert rel(x, xo) <= 1e-8
     # host callable preconditioner (Jacobi)
     dinv = 1.0 / A.diagonal()
     jac = lambda r: dinv * r  # noqa: E731
-    x, its, h = linsolve.cg(A, f, jac, tol=1e-8, max_iters=2000)
-    xo, itso, ho = ocg(A, f, jac, tol=1e-8, max_iters=2000)
+    x, its, h = linsolve.cg(A, fr, jac, tol=1e-8, max_iters=2000)
+    xo, itso, ho = ocg(A, fr, jac, tol=1e-8, max_iters=2000)
     assert its == itso
     assert np.max(np.abs(np.array(h) - ho)) / ho[0] <= 1e-10
     assert rel(x, xo) <= 1e-8
@@ -65,7 +68,8 @@ def test_cg_plain_host_callable_and_live_callback():
     assert [s[0] for s in seen] == list(range(1, its + 1))
     assert [s[1] for s in seen] == h
     xo, itso, ho = orc.solve(f)
-    assert its == itso and np.max(np.abs(np.array(h) - ho) / np.array(ho)) <= 1e-10
+    # the last entry of this one-level solve is 2e-16 (rounding noise): floor-aware comparison
+    assert its == itso and hist_ok(h, ho)[0], hist_ok(h, ho)
 
 
 def test_smoother_duck_type_matches_oracle():
@@ -113,7 +117,9 @@ def test_stationary_and_direct_iterates_match_oracle(mode):
     assert rep.iterations == itso and rep.converged == conv
     h, ho = np.array(rep.residuals), np.array(reso)
     assert np.max(np.abs(h - ho)) / ho[0] <= 1e-10
-    assert np.max(np.abs(h - ho) / ho) <= 1e-8
+    # residuals of the stationary iteration are f - A u recomputed from u: their absolute rounding
+    # noise is ~1e-13 of the first one, whatever their size
+    assert np.all(np.abs(h - ho) <= np.maximum(1e-8 * ho, 1e-13 * ho[0]))
     assert rel(rep.x, uo) <= 1e-9
 
 

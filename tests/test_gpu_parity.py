@@ -304,6 +304,48 @@ def test_flow_engine_matches_oracle(cfg, kw, G):
     solver.close()
 
 
+@pytest.mark.parametrize("cfg,kw,ctas", [("cfg5", {"levels": 2}, None), ("cfg5", {"levels": 2}, "64"),
+                                         ("cfg2", {"levels": 2}, None)])
+def test_wave_engine_matches_oracle(cfg, kw, ctas):
+    """IGB_GS_ENGINE=wave (opt-in): plane chains inside one CTA, external sums by the rest of the GPU
+    (wave.cu, wave_plan.cpp).  Every sweep 6x bitwise repeatable and within 1e-12 of SuperLU on
+    tril / triu, the PCG solve matches the oracle; with 64 CTAs the groups sweep several bundles
+    each (ticket hand-out, queue reuse)."""
+    import os
+    from paper_1902_01818_b200 import multigrid
+    from oracle.solve import OracleSolver
+    pr, setup, f = get_setup(cfg, **kw)
+    os.environ["IGB_GS_ENGINE"] = "wave"
+    if ctas:
+        os.environ["IGB_WAVE_CTAS"] = ctas
+    try:
+        solver = multigrid.MultigridSolver(pr.hier, pr.config, device=0, setup=setup)
+    finally:
+        del os.environ["IGB_GS_ENGINE"]
+        os.environ.pop("IGB_WAVE_CTAS", None)
+    orc = OracleSolver(setup.setup_bundle())
+    rng = np.random.default_rng(29)
+    engines = set()
+    for level in range(1, solver.finest + 1):
+        if orc.gs[level] is None:
+            continue
+        n = solver.A[level].shape[0]
+        x = rng.standard_normal(n)
+        for d, (op, ref) in enumerate((("gs_fwd", orc.gs_forward), ("gs_bwd", orc.gs_backward))):
+            engines.add(solver.ctx.gs_info(level, d)["engine"])
+            first = solver.ctx.op(op, level, x, n)
+            for _ in range(5):
+                assert np.array_equal(solver.ctx.op(op, level, x, n), first), (cfg, level, op)
+            assert rel(first, ref(level, x)) <= 1e-12, (cfg, level, op)
+    assert "wave" in engines
+    rep = solver.solve_pcg(f)
+    xo, itso, histo = orc.solve(f, tol=pr.config.tol, max_iters=pr.config.max_iters)
+    assert rep.iterations == itso
+    _check_history(rep.residuals, histo, f"{cfg} wave vs oracle", hist_tol(cfg))
+    assert rel(rep.x, xo) <= 1e-10
+    solver.close()
+
+
 @pytest.mark.parametrize("cfg,kw", [("cfg2", {"levels": 3}), ("cfg3", {"levels": 2}), ("cfg5", {"levels": 2}),
                                     ("cfg4", {"p": 4, "levels": 2})])
 def test_kronecker_transfers_match_P(cfg, kw):

@@ -1,0 +1,4 @@
+export PYTHONUNBUFFERED=1
+( time timeout 2400 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=15 ) > gpurun_out/r2_gpusuite.log 2>&1
+echo "rc=$?" >> gpurun_out/r2_gpusuite.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r2_smoke.log 2>&1; echo "rc=$?" >> gpurun_out/r2_smoke.log

@@ -204,6 +204,11 @@ int igb_profile_get(igb_ctx* ctx, int cls, double* ms, long long* launches, doub
 /* Algorithmic flops of a class since igb_profile_reset (the fast-diagonalisation class 2:
  * 4 prod(n) sum_a n_a per interior and application, i.e. 8 n^3 in 2-D, 12 n^4 in 3-D). */
 int igb_profile_flops(igb_ctx* ctx, int cls, double* flops);
+/* The class's largest launch since igb_profile_reset (most algorithmic bytes per launch: the
+ * finest level's kernel): accumulated time, count and the bytes of one such launch -- the launch
+ * an ncu capture of the class's dominant kernel shows, so roofline and traffic refer to the same
+ * thing (bench.py; no reference counterpart: measurement only). */
+int igb_profile_top(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes_per_launch);
 
 /* Which Gauss-Seidel engine igb_set_gs planned for (level, dir) (dir 0 forward, 1 backward);
  * info[0..ninfo) receives: engine (1 panel sweep, 2 flow sweep, 3 level-set sweep, 4 level

@@ -59,6 +59,7 @@ SIGNATURES = {
     "igb_smooth": ([_p, _i, _i, _i, _i, _p, _p], _i),
     "igb_cg": ([_p, _i, _ll, _p, _p, _p, _i, _p, _p, _p, _p, _p, _d, _i, _p, _ip, _p, _i], _i),
     "igb_profile_flops": ([_p, _i, ctypes.POINTER(_d)], _i),
+    "igb_profile_top": ([_p, _i, ctypes.POINTER(_d), ctypes.POINTER(_ll), ctypes.POINTER(_d)], _i),
 }
 PREC = {"none": 0, "cycle": 1, "host": 2}
 PREC_FN = ctypes.CFUNCTYPE(None, ctypes.POINTER(_d), ctypes.POINTER(_d), _i, _p)
@@ -288,7 +289,11 @@ class Context:
                         "igb_profile_get")
             fl = ctypes.c_double()
             self._check(self.lib.igb_profile_flops(self.h, k, ctypes.byref(fl)), "igb_profile_flops")
-            out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value, "flops": fl.value}
+            tms, tn, tby = ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
+            self._check(self.lib.igb_profile_top(self.h, k, ctypes.byref(tms), ctypes.byref(tn), ctypes.byref(tby)),
+                        "igb_profile_top")
+            out[name] = {"ms": ms.value, "launches": n.value, "bytes": by.value, "flops": fl.value,
+                         "top": {"ms": tms.value, "launches": tn.value, "bytes_per_launch": tby.value}}
         return out
 
     def gs_info(self, level, direction):

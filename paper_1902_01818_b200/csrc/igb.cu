@@ -260,6 +260,9 @@ struct igb_ctx {
   long long prof_n[K_NCLASS] = {0};
   double prof_bytes[K_NCLASS] = {0};
   double prof_flops[K_NCLASS] = {0};
+  // the class's largest launch (most algorithmic bytes: the finest level's kernel)
+  double top_bytes[K_NCLASS] = {0}, top_ms[K_NCLASS] = {0};
+  long long top_n[K_NCLASS] = {0};
 
   // timing of last pcg
   double last_pcg_ms = 0, last_cycle_ms = 0;
@@ -347,6 +350,15 @@ struct igb_ctx {
       prof_n[r.cls] += 1;
       prof_bytes[r.cls] += r.bytes;
       prof_flops[r.cls] += r.flops;
+      if (r.bytes > top_bytes[r.cls] * (1.0 + 1e-9)) {
+        top_bytes[r.cls] = r.bytes;
+        top_ms[r.cls] = 0;
+        top_n[r.cls] = 0;
+      }
+      if (r.bytes >= top_bytes[r.cls] * (1.0 - 1e-9)) {
+        top_ms[r.cls] += ms;
+        top_n[r.cls] += 1;
+      }
     }
     if (clear) {
       recs.clear();
@@ -2736,6 +2748,8 @@ int igb_profile_reset(igb_ctx* ctx) {
       ctx->prof_n[c] = 0;
       ctx->prof_bytes[c] = 0;
       ctx->prof_flops[c] = 0;
+      ctx->top_bytes[c] = ctx->top_ms[c] = 0;
+      ctx->top_n[c] = 0;
     }
   });
 }
@@ -2753,6 +2767,15 @@ int igb_profile_flops(igb_ctx* ctx, int cls, double* flops) {
   return guarded(ctx, [&] {
     if (cls < 0 || cls >= K_NCLASS) throw ArgError("unknown kernel class");
     if (flops) *flops = ctx->prof_flops[cls];
+  });
+}
+
+int igb_profile_top(igb_ctx* ctx, int cls, double* ms, long long* launches, double* bytes_per_launch) {
+  return guarded(ctx, [&] {
+    if (cls < 0 || cls >= K_NCLASS) throw ArgError("unknown kernel class");
+    if (ms) *ms = ctx->top_ms[cls];
+    if (launches) *launches = ctx->top_n[cls];
+    if (bytes_per_launch) *bytes_per_launch = ctx->top_bytes[cls];
   });
 }
 

@@ -989,7 +989,10 @@ void require_final(igb_ctx* ctx) {
 
 void build_fd_plan(igb_ctx* ctx, Level& V) {
   if (V.interiors.empty()) return;
-  int dim = V.interiors[0].dim;
+  // the level's dimension; a 3-D level may also carry 2-D items: faces between patches whose piece
+  // matrix has tensor form are applied by 2-D fast diagonalisation (smoothers.py: _tensor_face)
+  int dim = 2;
+  for (auto& it : V.interiors) dim = std::max(dim, it.dim);
   V.fd.flops = 0.0;
   for (auto& it : V.interiors) {  // 2 d contractions (front + back), 2 flops per FMA
     const double cells = (double)it.n[0] * it.n[1] * (it.dim == 3 ? it.n[2] : 1);
@@ -1001,9 +1004,10 @@ void build_fd_plan(igb_ctx* ctx, Level& V) {
   static const bool large_ok = !(std::getenv("IGB_FD_LARGE") && std::atoi(std::getenv("IGB_FD_LARGE")) == 0);
   const bool fuse = !(std::getenv("IGB_FD_FUSE") && std::string(std::getenv("IGB_FD_FUSE")) == "0");
   for (auto& it : V.interiors) {
-    if (it.dim != dim) throw ArgError("mixed interior dimensions on one level");
-    if (fuse && dim == 2 && it.n[0] <= FDC_NMAX && it.n[1] <= FDC_NMAX) {
+    if (it.dim == 2 && (fuse || dim == 3) && it.n[0] <= FDC_NMAX && it.n[1] <= FDC_NMAX) {
       clu.push_back(FdCluster{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]});
+    } else if (it.dim == 2 && dim == 3) {
+      throw ArgError("2-D items of a 3-D level must fit the fused 2-D kernels (sides <= 160)");
     } else if (fuse && large_ok && dim == 2 && it.n[0] <= FDL_NMAX && it.n[1] <= FDL_NMAX) {
       clu_large.push_back(FdCluster{it.T[0], it.T[1], it.D, it.idx, nullptr, it.n[0], it.n[1]});
     } else {

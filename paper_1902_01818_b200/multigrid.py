@@ -235,8 +235,12 @@ class MultigridSolver:
                 for piece, solver in scms.interiors:
                     ctx.scms_add_interior(level, solver.dims, solver.square_transforms,
                                           solver.denominator, piece.indices)
-                for (piece, _), inv in zip(scms.pieces, scms.piece_inverses):
-                    ctx.scms_add_piece(level, piece.indices, inv)
+                for i, ((piece, _), inv) in enumerate(zip(scms.pieces, scms.piece_inverses)):
+                    if i in scms.tensor_faces:   # 3-D face with tensor structure: 2-D fast diagonalisation
+                        fdims, fV, fden = scms.tensor_faces[i]
+                        ctx.scms_add_interior(level, fdims, fV, fden, piece.indices)
+                    else:
+                        ctx.scms_add_piece(level, piece.indices, inv)
                 lap(f"scms level {level}")
             if gs is not None:  # after the interiors (only the opt-in KF 10 panel variant reads the dimension)
                 ctx.set_gs(level)

@@ -21,6 +21,8 @@ Device data produced here:
 
 from dataclasses import dataclass, field
 
+import os
+
 import numpy as np
 import scipy.linalg
 import scipy.sparse
@@ -376,6 +378,59 @@ class ScmsInteriorSolver:
         return self._square[1]
 
 
+def _tensor_face(sub, piece, hier, level, tol=1e-13, nmax=160):
+    """Fast diagonalisation of a 3-D face piece, when its matrix has the tensor form.
+
+    The reference solves every interface piece with SuperLU on the principal submatrix
+    ``A[idx][:, idx]`` (``smoothers.py:316-319``).  On conforming affine patches the face between
+    two patches is a 2-D tensor grid and that submatrix is
+        a M1 (x) M2 + b1 K1 (x) M2 + b2 M1 (x) K2
+    (M_i, K_i: interior blocks of the tangential 1-D mass / stiffness matrices; a, b_i collect the
+    normal direction's boundary entries of both patches).  Then, with K_i V_i = M_i V_i L_i and
+    V_i^T M_i V_i = I,
+        sub^-1 R = V1 ((V1^T R V2) ./ (a + b1 l1_j + b2 l2_k)) V2^T,
+    which the device applies with the interiors' 2-D kernels instead of streaming a dense m x m
+    inverse (cfg5: twelve 4225^2 inverses = 1.7 GB per application).  The form is *fitted and
+    verified numerically* (max |sub - fit| <= tol max |sub|); anything else keeps the dense
+    inverse.  Returns (dims, [V1, V2], denominator) or None."""
+    import scipy.linalg as sla
+    import scipy.sparse as sp
+    from . import bspline
+    if hier.dim != 3 or piece.kind != "face":
+        return None
+    iface = hier.domain.interfaces[piece.entity[1]]
+    k, axis = iface.k, iface.side_k.axis
+    spaces = hier.spaces[level][k]
+    tang = [a for a in range(3) if a != axis]
+    Ms = [bspline.interior_matrix(bspline.univariate_mass(spaces[a])).tocsr() for a in tang]
+    Ks = [bspline.interior_matrix(bspline.univariate_stiffness(spaces[a])).tocsr() for a in tang]
+    dims = tuple(M.shape[0] for M in Ms)
+    if dims[0] * dims[1] != sub.shape[0] or max(dims) > nmax or min(dims) < 1:
+        return None
+    basis = [sp.kron(Ms[0], Ms[1], format="csr"), sp.kron(Ks[0], Ms[1], format="csr"),
+             sp.kron(Ms[0], Ks[1], format="csr")]
+    S = sub.tocsr()
+    G = np.array([[bi.multiply(bj).sum() for bj in basis] for bi in basis])
+    rhs = np.array([bi.multiply(S).sum() for bi in basis])
+    try:
+        coef = np.linalg.solve(G, rhs)
+    except np.linalg.LinAlgError:
+        return None
+    fit = coef[0] * basis[0] + coef[1] * basis[1] + coef[2] * basis[2]
+    err = abs(S - fit).max()
+    if not err <= tol * abs(S).max():
+        return None
+    lam, V = [], []
+    for M, K in zip(Ms, Ks):
+        w, v = sla.eigh(K.toarray(), M.toarray())
+        lam.append(w)
+        V.append(np.ascontiguousarray(v))
+    denom = coef[0] + coef[1] * lam[0][:, None] + coef[2] * lam[1][None, :]
+    if not np.all(denom > 0):
+        return None
+    return dims, V, np.ascontiguousarray(denom)
+
+
 class SubspaceCorrectedMass(_DeviceBound):
     """Damped additive piece-local solves of one level (``smoothers.py:297-332``)."""
 
@@ -389,6 +444,7 @@ class SubspaceCorrectedMass(_DeviceBound):
         self.decomposition = build_piece_decomposition(hier, level)
         self.interiors = []      # (piece, ScmsInteriorSolver)
         self.pieces = []         # (piece, Factorization)
+        self.tensor_faces = {}   # index into pieces -> (dims, [V1, V2], denominator): see _tensor_face
         cache = {}
         A = A.tocsr()
         for piece in self.decomposition.pieces:
@@ -402,13 +458,22 @@ class SubspaceCorrectedMass(_DeviceBound):
             else:
                 sub = A[piece.indices][:, piece.indices].tocsc()
                 self.pieces.append((piece, linsolve.factorize(sub, spd=True)))
+                if os.environ.get("IGB_TENSOR_FACES", "1") != "0":
+                    fd = _tensor_face(sub, piece, hier, level)
+                    if fd is not None:
+                        self.tensor_faces[len(self.pieces) - 1] = fd
         self._inverses = None
 
     @property
     def piece_inverses(self):
-        """Dense inverses of the interface principal submatrices (from the SuperLU factors)."""
+        """Dense inverses of the interface principal submatrices (from the SuperLU factors); None for
+        the faces applied by fast diagonalisation (``tensor_faces``)."""
         if self._inverses is None:
-            self._inverses = linsolve.inverses([fact for _, fact in self.pieces])
+            dense = [i for i in range(len(self.pieces)) if i not in self.tensor_faces]
+            inv = linsolve.inverses([self.pieces[i][1] for i in dense])
+            self._inverses = [None] * len(self.pieces)
+            for i, m in zip(dense, inv):
+                self._inverses[i] = m
         return self._inverses
 
     def apply(self, r):

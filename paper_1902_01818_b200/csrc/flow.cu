@@ -60,6 +60,9 @@ __device__ __forceinline__ double ld_f64_volatile(const double* p) {
   asm volatile("ld.global.f64 %0, [%1];" : "=d"(v) : "l"(p));
   return v;
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ bool is_pending(double v) {
   return (unsigned long long)__double_as_longlong(v) == FLOW_PENDING;
 }
@@ -86,15 +89,18 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
   const long long stride = nwarps * RPW;
 
   long long q0 = gwarp * RPW;
-  int nrow = -1, ns = 0, ne = 0;
+  int nrow = -1, ns = 0, ne = 0, ncc = -1, nel = -1;
   if (q0 < a.nq) {
     nrow = ld_nc_s32(a.row + q0 + sub);
     ns = ld_nc_s32(a.eptr + q0 + sub);
     ne = ld_nc_s32(a.eptr + q0 + sub + 1);
+    if (a.crit) ncc = ld_nc_s32(a.crit + q0 + sub);
+    if (a.elate) nel = ld_nc_s32(a.elate + q0 + sub);
   }
   for (; q0 < a.nq; q0 += stride) {
     const long long q = q0 + sub;
-    const int row = nrow, s = ns, e = ne;
+    const int row = nrow, s = ns, e = ne, cc = ncc;
+    const int el = (a.elate && row >= 0) ? nel : e;  // early entries [s, el)
     long long c0 = 0, t0 = 0;
     if (a.trace && gl == 0) {
       t0 = gtime();
@@ -110,9 +116,34 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
       nrow = ld_nc_s32(a.row + q + stride);
       ns = ld_nc_s32(a.eptr + q + stride);
       ne = ld_nc_s32(a.eptr + q + stride + 1);
+      if (a.crit) ncc = ld_nc_s32(a.crit + q + stride);
+      if (a.elate) nel = ld_nc_s32(a.elate + q + stride);
+      // ... and its entries, right-hand side and old value into L2: a row is a chain of memory round
+      // trips (entries -> values -> late entries -> late values), and on wide levels (cfg5's finest:
+      // 733 rows per level for 2,368 warps) the sweep is bound by the time a warp spends per row;
+      // with the coefficient stream already in L2 two of those trips cost 0.3 us instead of ~1.2
+      if (a.prefetch) {
+        const char* pc = reinterpret_cast<const char*>(a.ecol + ns);
+        const char* pv = reinterpret_cast<const char*>(a.eval + ns);
+        const int bc = (ne - ns) * 4;
+        for (int o = gl * 128; o < bc; o += G * 128) prefetch_l2(pc + o);
+        for (int o = gl * 128; o < 2 * bc; o += G * 128) prefetch_l2(pv + o);
+        if (gl == 0 && nrow >= 0) {
+          prefetch_l2(a.res + nrow);
+          if (a.accumulate) prefetch_l2(a.u + nrow);
+        }
+      }
+    }
+    // first chunk of the row's coefficients: in flight while the critical dependency is awaited
+    int c[K];
+    double v[K], x[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int idx = s + gl + k * G;
+      c[k] = idx < el ? __ldcs(a.ecol + idx) : -1;
+      v[k] = idx < el ? __ldcs(a.eval + idx) : 0.0;
     }
     if (a.crit && gl == 0 && row >= 0) {  // wait for the latest dependency first (one poller per row)
-      const int cc = ld_nc_s32(a.crit + q);
       if (cc >= 0 && is_pending(ld_relaxed(xg_cur + cc))) {
         const long long w0 = clock64();
         while (is_pending(ld_relaxed(xg_cur + cc))) {
@@ -125,15 +156,14 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
     long long cc0 = 0;
     if (a.trace && gl == 0) cc0 = clock64();
     double acc = 0.0;
-    const int el = (a.elate && row >= 0) ? ld_nc_s32(a.elate + q) : e;  // early entries [s, el)
     for (int base = s; base < el; base += G * K) {
-      int c[K];
-      double v[K], x[K];
+      if (base > s) {
 #pragma unroll
-      for (int k = 0; k < K; ++k) {
-        const int idx = base + gl + k * G;
-        c[k] = idx < el ? __ldcs(a.ecol + idx) : -1;
-        v[k] = idx < el ? __ldcs(a.eval + idx) : 0.0;
+        for (int k = 0; k < K; ++k) {
+          const int idx = base + gl + k * G;
+          c[k] = idx < el ? __ldcs(a.ecol + idx) : -1;
+          v[k] = idx < el ? __ldcs(a.eval + idx) : 0.0;
+        }
       }
 #pragma unroll
       for (int k = 0; k < K; ++k) x[k] = c[k] >= 0 ? ld_relaxed(xg_cur + c[k]) : 0.0;

@@ -1781,8 +1781,25 @@ bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   // IGB_FLOW_CRITLAG / IGB_FLOW_LATE override both directions (IGB_FLOW_LATE=0: one batch).
   const char* le = std::getenv("IGB_FLOW_CRITLAG");
   const char* lm = std::getenv("IGB_FLOW_LATE");
-  const int lag = le ? std::max(1, std::atoi(le)) : (dir ? 4 : 8);
-  const int late_max = lm ? std::max(0, std::atoi(lm)) : (dir ? 32 : 64);
+  int lag = le ? std::max(1, std::atoi(le)) : (dir ? 4 : 8);
+  int late_max = lm ? std::max(0, std::atoi(lm)) : (dir ? 32 : 64);
+  {
+    // Wide levels (cfg5's finest: 733 rows per dependency level for 2,368 resident warps, ~3 levels
+    // in flight) are bound by the time a warp spends per row, not by the hop: a trace shows 2.7 of
+    // 4.9 us per row in the serial late tail (profiles/r2_flow_trace_cfg5.log).  With so few levels
+    // in flight only the dependencies of the last few levels can still be pending, so the lag
+    // shrinks to that window and the tail to one chunk.  IGB_FLOW_WIDE_LAG / _LATE / _INFLIGHT tune it.
+    const Sched& Sd = dir ? V.bwd : V.fwd;
+    const double width = double(V.n) / std::max(1, Sd.nlev);
+    const double in_flight = flow_max_ctas() * (FLOW_NT / 32.0) / std::max(1.0, width);
+    const char* wt = std::getenv("IGB_FLOW_WIDE_INFLIGHT");
+    const char* wl = std::getenv("IGB_FLOW_WIDE_LAG");
+    const char* wm = std::getenv("IGB_FLOW_WIDE_LATE");
+    if (!le && !lm && in_flight < (wt ? std::atof(wt) : 6.0)) {
+      lag = wl ? std::max(1, std::atoi(wl)) : 3;
+      late_max = wm ? std::max(0, std::atoi(wm)) : 8;
+    }
+  }
   if (!build_flow_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,
                        ge ? std::atoi(ge) : 0, late_max > 0 ? lag : (le ? lag : 2), late_max, plan))
     return false;
@@ -1802,6 +1819,8 @@ bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   if (late_max > 0) a.elate = ctx->upload(plan.elate.data(), plan.elate.size());
   const char* be = std::getenv("IGB_FLOW_BACKOFF");
   a.backoff = be ? std::atoi(be) : 0;
+  const char* pfe = std::getenv("IGB_FLOW_PREFETCH");
+  a.prefetch = pfe ? std::atoi(pfe) : 1;
   std::vector<unsigned long long> pend((size_t)2 * V.n, 0x7FF4DEADBEEF5678ULL);  // flow.cu FLOW_PENDING
   a.xg = reinterpret_cast<double*>(ctx->upload(pend.data(), pend.size()));
   int* ctr = ctx->alloc<int>(2);

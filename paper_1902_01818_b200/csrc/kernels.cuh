@@ -158,6 +158,7 @@ struct FlowArgs {
   const int* elate;    // [nq] first late entry of the row (flow_plan.h): early entries are reduced
                        // first, the late ones (newest dependencies) added serially by every lane
   int backoff;         // ns slept between polls of crit (0: spin)
+  int prefetch;        // L2-prefetch the next row's entries while the current row is processed
   long long* trace;    // debug (nullable): per slot globaltimer at start / deps ready / stored
 };
 int flow_max_ctas();  // co-resident CTAs of FLOW_NT threads (all variants)

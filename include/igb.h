@@ -117,7 +117,11 @@ int igb_scms_begin(igb_ctx* ctx, int level, double tau);
  * (columns = eigenvectors of the split subspaces, [W_L V_L | W_C V_C]);
  * denom has prod(n_a) entries (C order); idx maps the C-order tensor to free ids.
  * T2 is ignored when dim == 2. Interiors whose T / denom have identical content share one device
- * copy (content-hashed and compared; buffers are copied during the call and may be reused). */
+ * copy (content-hashed and compared; buffers are copied during the call and may be reused).
+ * Any index set whose piece operator has this tensor form may be passed: a 3-D level also takes
+ * dim == 2 items (sides <= 160) -- the faces between conforming affine patches, whose SuperLU solve
+ * (reference smoothers.py:316-319) equals X = V1 ((V1^T R V2) ./ denom) V2^T with the generalized
+ * eigenvectors of the tangential 1-D stiffness / mass pairs. */
 int igb_scms_add_interior(igb_ctx* ctx, int level, int dim, const int* dims,
                           const double* T0, const double* T1, const double* T2,
                           const double* denom, const int* idx);

@@ -106,6 +106,10 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
       t0 = gtime();
       c0 = clock64();
     }
+    // first probe of the critical dependency: its L2 round trip runs under the loads issued below
+    double cv = 0.0;
+    const bool crit_wait = a.crit && gl == 0 && row >= 0 && cc >= 0;
+    if (crit_wait) cv = ld_relaxed(xg_cur + cc);
     double rhs = 0.0, uold = 0.0, idg = 0.0;
     if (gl == 0 && row >= 0) {
       rhs = ld_nc_f64(a.res + row);
@@ -143,8 +147,8 @@ __global__ void __launch_bounds__(FLOW_NT, FLOW_MINB) flow_sweep_kernel(FlowArgs
       c[k] = idx < el ? __ldcs(a.ecol + idx) : -1;
       v[k] = idx < el ? __ldcs(a.eval + idx) : 0.0;
     }
-    if (a.crit && gl == 0 && row >= 0) {  // wait for the latest dependency first (one poller per row)
-      if (cc >= 0 && is_pending(ld_relaxed(xg_cur + cc))) {
+    if (crit_wait) {  // wait for the latest dependency first (one poller per row)
+      if (is_pending(cv)) {
         const long long w0 = clock64();
         while (is_pending(ld_relaxed(xg_cur + cc))) {
           if (a.backoff) __nanosleep(a.backoff);

@@ -1784,20 +1784,18 @@ bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
   int lag = le ? std::max(1, std::atoi(le)) : (dir ? 4 : 8);
   int late_max = lm ? std::max(0, std::atoi(lm)) : (dir ? 32 : 64);
   {
-    // Wide levels (cfg5's finest: 733 rows per dependency level for 2,368 resident warps, ~3 levels
-    // in flight) are bound by the time a warp spends per row, not by the hop: a trace shows 2.7 of
-    // 4.9 us per row in the serial late tail (profiles/r2_flow_trace_cfg5.log).  With so few levels
-    // in flight only the dependencies of the last few levels can still be pending, so the lag
-    // shrinks to that window and the tail to one chunk.  IGB_FLOW_WIDE_LAG / _LATE / _INFLIGHT tune it.
-    const Sched& Sd = dir ? V.bwd : V.fwd;
-    const double width = double(V.n) / std::max(1, Sd.nlev);
-    const double in_flight = flow_max_ctas() * (FLOW_NT / 32.0) / std::max(1.0, width);
-    const char* wt = std::getenv("IGB_FLOW_WIDE_INFLIGHT");
-    const char* wl = std::getenv("IGB_FLOW_WIDE_LAG");
-    const char* wm = std::getenv("IGB_FLOW_WIDE_LATE");
-    if (!le && !lm && in_flight < (wt ? std::atof(wt) : 6.0)) {
-      lag = wl ? std::max(1, std::atoi(wl)) : 3;
-      late_max = wm ? std::max(0, std::atoi(wm)) : 8;
+    // Rows served by a whole warp (G = 32: 3-D stencils, > 56 entries per row): crit lag 3, one late
+    // chunk.  A per-row trace of cfg5's finest sweep (733 rows per dependency level for 2,368
+    // resident warps, ~3 levels in flight: bound by the time a warp spends per row, not by the hop)
+    // showed 2.7 of 4.9 us per row in the serial late tail of the lag-8 split
+    // (profiles/r2_flow_trace_cfg5.log); with the next row's entries prefetched into L2 and the
+    // first chunk in flight during the crit wait the short lag is also the best choice on the
+    // narrow levels (cfg5 full, whole solve: lag 8 / 4 everywhere 104.9 ms, lag 3 on the finest level
+    // 89.0, on levels 3-4 87.3, on every level 85.8).  IGB_FLOW_CRITLAG / IGB_FLOW_LATE override.
+    const long long tri = dir ? V.tri_nnz_upper : V.tri_nnz_lower;
+    if (!le && !lm && tri > 56LL * V.n) {
+      lag = 3;
+      late_max = 8;
     }
   }
   if (!build_flow_plan(V.n, V.h_ptr.data(), V.h_col.data(), V.h_val.data(), dp.data(), dir == 1,

@@ -108,7 +108,9 @@ int igb_set_prolongation_kron(igb_ctx* ctx, int level, int dim, int npatch, cons
 int igb_set_matrix_free(igb_ctx* ctx, int level, int dim, int npatch, int p, const int* dims, const double* c,
                         const double* Mband, const double* Kband, const int* block_free);
 
-/* Gauss-Seidel on A_l in natural order (level schedules are built here). */
+/* Gauss-Seidel on A_l in natural order (level schedules are built here).  Call it after the
+ * level's igb_scms_add_interior calls when the smoother is hybrid: the sweep planner tunes the flow
+ * sweep's early / late split by the level's dimension (results do not depend on it, only speed). */
 int igb_set_gs(igb_ctx* ctx, int level);
 
 /* SCMS smoother of level l: damping tau; then interiors and interface pieces. */

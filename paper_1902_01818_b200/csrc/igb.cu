@@ -1792,8 +1792,11 @@ bool build_flow_sweep(igb_ctx* ctx, Level& V, int level, int dir, const std::vec
     // first chunk in flight during the crit wait the short lag is also the best choice on the
     // narrow levels (cfg5 full, whole solve: lag 8 / 4 everywhere 104.9 ms, lag 3 on the finest level
     // 89.0, on levels 3-4 87.3, on every level 85.8).  IGB_FLOW_CRITLAG / IGB_FLOW_LATE override.
+    // 3-D levels only (known once the level's interiors are registered): on cfg4 p = 8's 2-D
+    // backward levels (145 entries per row) the old lag 4 / 32 stays better (264.5 vs 279.3 ms).
     const long long tri = dir ? V.tri_nnz_upper : V.tri_nnz_lower;
-    if (!le && !lm && tri > 56LL * V.n) {
+    const bool three_d = !V.interiors.empty() && V.interiors[0].dim == 3;
+    if (!le && !lm && three_d && tri > 56LL * V.n) {
       lag = 3;
       late_max = 8;
     }

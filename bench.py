@@ -15,7 +15,9 @@ checked against the reference's (EXPECTED_ITS) and the line fails on a mismatch.
   e2e    = same metric through the public host API (Context.pcg: pinned-host b -> device,
            solve, x -> host), wall clock per step;
   roofline = dominant kernel class from a separate profiled pass (CUDA events around every
-           launch, same K steps) -> algorithmic bytes / mean launch time vs MEASURED_PEAKS.json;
+           launch, same K steps): the class's largest launch (the finest-level kernel,
+           igb_profile_top) -> its algorithmic bytes / its mean time vs MEASURED_PEAKS.json, and
+           traffic = the DRAM bytes ncu shows for the same launch (profiles/traffic.json);
   roofline_fd = the fast-diagonalisation class's flops / time vs the measured fp64 DGEMM peak
            (profiles/r2_fp64_peak.json; MEASURED_PEAKS.json has no fp64 entry);
   cpu_baseline = oracle/ (reference-faithful NumPy/SciPy restatement) on a bounded sample.

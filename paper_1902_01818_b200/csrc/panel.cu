@@ -440,7 +440,7 @@ void launch_one(cudaStream_t st, const PanelArgs& a) {
 }
 
 // variants: B = 512: KA in {2,4,8,12}, KF in {0,1,4}, and KA 14 with KF 0;  B = 256: KA in {4,8,12},
-// KF in {0,4,8}
+// KF in {0,4,8}, and KA 14 with KF 0 / 4, KA 18 with KF 0
 template <int KA>
 void dispatch_kf17(cudaStream_t st, const PanelArgs& a) {
   switch (a.KF) {
@@ -491,6 +491,11 @@ void for_all_variants(int KBC, F&& f) {
   if (KBC == 17) f(panel_sweep_kernel<17, 14, 0>);  // long single-range rows (p = 8 backward: ~208 near)
   if (KBC == 17) f(panel_sweep_kernel<17, 8, 5>);   // p = 6 backward: up to 78 far entries per row
   if (KBC == 9) f(panel_sweep_kernel<9, 12, 10>);   // p = 8 backward, several ranges: 136 far entries
+  if (KBC == 9) {  // small 3-D levels: interface rows with up to 279 near entries
+    f(panel_sweep_kernel<9, 14, 0>);
+    f(panel_sweep_kernel<9, 14, 4>);
+    f(panel_sweep_kernel<9, 18, 0>);
+  }
 }
 
 }  // namespace
@@ -576,6 +581,11 @@ void launch_panel_sweep(cudaStream_t st, const PanelArgs& a) {
     switch (a.KA) {
       case 4: dispatch_kf9<4>(st, a); break;
       case 8: dispatch_kf9<8>(st, a); break;
+      case 14:
+        if (a.KF == 0) launch_one<9, 14, 0>(st, a);
+        else launch_one<9, 14, 4>(st, a);
+        break;
+      case 18: launch_one<9, 18, 0>(st, a); break;
       default: dispatch_kf9<12>(st, a); break;
     }
   }

@@ -157,7 +157,7 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
     out.far_entries += nf;
   }
   out.KA = W == 16 ? round_up_variant((max_near + 15) / 16, {2, 4, 8, 12, 14})
-                   : round_up_variant((max_near + 15) / 16, {4, 8, 12});
+                   : round_up_variant((max_near + 15) / 16, {4, 8, 12, 14, 18});
   out.KF = W == 16 ? round_up_variant((max_far + 15) / 16, {0, 1, 4, 5})
                    : (allow_kf10 ? round_up_variant((max_far + 15) / 16, {0, 4, 8, 10})
                                  : round_up_variant((max_far + 15) / 16, {0, 4, 8}));
@@ -165,7 +165,12 @@ bool build_panel_plan(int n, const int* ptr, const int* col, const double* val, 
     if (out.KA > 12) out.KF = -1;  // KF 10 exists with KA 12 only
     else out.KA = 12;
   }
-  if (out.KA == 14 && out.KF != 0) out.KA = -1;  // the KA 14 variant exists without far slots only
+  if (W == 16 && out.KA == 14 && out.KF != 0) out.KA = -1;  // B = 512: the KA 14 variant exists without far slots only
+  // B = 256 long-row variants (interface rows of small 3-D levels: up to 279 near entries backward):
+  // KA 14 with KF 0 / 4, KA 18 with KF 0
+  if (W == 8 && out.KA == 14 && out.KF > 4) out.KA = -1;
+  if (W == 8 && out.KA == 14 && out.KF > 0) out.KF = 4;
+  if (W == 8 && out.KA == 18 && out.KF != 0) out.KA = -1;
   if (out.KF == 5 && out.KA > 8) out.KF = -1;     // KF 5 exists with KA <= 8 only
   if (out.KF == 5) out.KA = 8;
   if (out.KA < 0 || out.KF < 0) {
